@@ -1,0 +1,253 @@
+"""ctypes driver for the C restatement of the reference hot path.
+
+TEST INFRASTRUCTURE ONLY -- the parity oracle.  Only tests/, the
+``__graft_entry__.smoke()`` check and bench.py's CPU-baseline leg import this
+module, and only as the checker or the timed CPU baseline; the product
+(`paper_1806_04960_b200`) never imports it and has no CPU fallback.
+
+``OracleSimulation`` restates ``wbflow.timestepper.Simulation``
+(pkg/src/wbflow/timestepper.py:48-229): same double buffer, same step order
+(prepare -> dt -> reconstruct -> x/y sweeps -> update -> swap), same error
+messages, step/cell context and "failed step is not committed" rule, with
+all numerics in oracle/liboracle.so (wb_oracle.c).
+"""
+
+import ctypes
+import os
+import subprocess
+import time
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+_U8 = ctypes.POINTER(ctypes.c_uint8)
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int),
+                ("dx", ctypes.c_double), ("dy", ctypes.c_double),
+                ("k0", ctypes.c_double), ("rho0", ctypes.c_double),
+                ("gamma", ctypes.c_double), ("g", ctypes.c_double),
+                ("eps", ctypes.c_double),
+                ("bcw", ctypes.c_int), ("bce", ctypes.c_int),
+                ("bcs", ctypes.c_int), ("bcn", ctypes.c_int),
+                ("kind_l", ctypes.c_int), ("kind_r", ctypes.c_int),
+                ("kind_b", ctypes.c_int), ("kind_t", ctypes.c_int),
+                ("seg_l", ctypes.c_double * 2), ("seg_r", ctypes.c_double * 2),
+                ("seg_b", ctypes.c_double * 2), ("seg_t", ctypes.c_double * 2),
+                ("in_l", ctypes.c_double * 4), ("in_r", ctypes.c_double * 4),
+                ("in_b", ctypes.c_double * 4), ("in_t", ctypes.c_double * 4)]
+
+
+def build():
+    """Compile liboracle.so with the committed Makefile (gcc, -ffp-contract=off)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            build()
+        _lib = ctypes.CDLL(_LIB)
+        _lib.wbo_tait_p.restype = ctypes.c_double
+        _lib.wbo_sound_c2.restype = ctypes.c_double
+        _lib.wbo_eq_rho.restype = ctypes.c_double
+        for f in ("wbo_tait_p", "wbo_sound_c2"):
+            getattr(_lib, f).argtypes = [ctypes.c_double] * 4
+        _lib.wbo_eq_rho.argtypes = [ctypes.c_double] * 5
+    return _lib
+
+
+def _p(a):
+    if a.dtype == np.uint8:
+        return a.ctypes.data_as(_U8)
+    return a.ctypes.data_as(_D)
+
+
+def set_threads(n):
+    lib().wbo_set_threads(int(n))
+
+
+def num_threads():
+    return lib().wbo_num_threads()
+
+
+# ---- scalar kernels (unit-level parity) ---------------------------------
+
+def eq_rho(y, y0, k0, rho0, g):
+    return lib().wbo_eq_rho(y, y0, k0, rho0, g)
+
+
+def tait_p(rho, k0, rho0, gamma):
+    return lib().wbo_tait_p(rho, k0, rho0, gamma)
+
+
+def osher_x_edge(qm, qp, k0, rho0, gamma):
+    qm = np.ascontiguousarray(qm, dtype=np.float64)
+    qp = np.ascontiguousarray(qp, dtype=np.float64)
+    out = np.zeros(10)
+    lib().wbo_osher_x_edge(_p(qm), _p(qp), ctypes.c_double(k0), ctypes.c_double(rho0),
+                           ctypes.c_double(gamma), _p(out))
+    return out
+
+
+def or_y_edge(qm, qp, y0, aeq, k0, rho0, gamma, g):
+    qm = np.ascontiguousarray(qm, dtype=np.float64)
+    qp = np.ascontiguousarray(qp, dtype=np.float64)
+    out = np.zeros(10)
+    lib().wbo_or_y_edge(_p(qm), _p(qp), *(ctypes.c_double(v) for v in
+                                          (y0, aeq, k0, rho0, gamma, g)), _p(out))
+    return out
+
+
+# ---- time stepper ------------------------------------------------------------
+
+class OracleError(RuntimeError):
+    def __init__(self, message, step=None, cell=None):
+        text = message
+        if step is not None:
+            text += f" (step {step})"
+        if cell is not None:
+            text += f" at cell {cell}"
+        super().__init__(text)
+        self.base = message
+        self.step = step
+        self.cell = cell
+
+
+def _inflow(cond):
+    if cond.kind != "inflow":
+        return (0.0, 0.0, 0.0, 0.0)
+    w = np.asarray(cond.state, dtype=np.float64)
+    ar = w[3] * w[0]
+    return (ar, ar * w[1], ar * w[2], w[3])
+
+
+_KIND = {"reflective": 1, "transmissive": 2, "inflow": 3}
+
+
+class OracleSimulation:
+    """CPU oracle with the reference ``Simulation`` semantics."""
+
+    def __init__(self, grid, params, q0, boundary, cfl=0.45):
+        if not 0.0 < cfl < 1.0:
+            raise OracleError(f"cfl must lie in (0, 1), got {cfl}")
+        self.grid, self.params, self.boundary, self.cfl = grid, params, boundary, float(cfl)
+        nx, ny = grid.nx, grid.ny
+        self.q = np.ascontiguousarray(np.array(q0, dtype=np.float64))
+        assert self.q.shape == (nx, ny, 5)
+        self.q_next = np.zeros_like(self.q)
+        self.t = 0.0
+        self.step_count = 0
+        self.mask = np.ascontiguousarray(grid.mask, dtype=np.uint8)
+        self.ycent = np.ascontiguousarray(grid.y_centers)
+        self.yfaces = np.ascontiguousarray(grid.y_faces)
+        self.xcent = np.ascontiguousarray(grid.x_centers)
+        self.y0s = np.zeros(nx)
+        self.aeqs = np.ones(nx)
+        self.y0s_prev = np.full(nx, np.nan)
+        self.col_rate = np.zeros(nx)
+        self.rhoE_c = np.zeros((nx, ny))
+        self.rhoE_fy = np.zeros((nx, ny + 1))
+        self.quiet = np.zeros((nx, ny), dtype=np.uint8)
+        self.flags = np.zeros((nx, ny), dtype=np.uint8)
+        for name in ("psi", "fW", "fE", "fS", "fN", "vol", "DW", "DE", "DS", "DN"):
+            setattr(self, name, np.zeros((nx, ny, 5)))
+        c = _Cfg()
+        c.nx, c.ny, c.dx, c.dy = nx, ny, grid.dx, grid.dy
+        c.k0, c.rho0, c.gamma, c.g, c.eps = (params.k0, params.rho0, params.gamma,
+                                            params.g, params.epsilon)
+        sides = [boundary.side(s) for s in ("left", "right", "bottom", "top")]
+        c.bcw, c.bce, c.bcs, c.bcn = (1 if s.kind == "reflective" else 2 for s in sides)
+        c.kind_l, c.kind_r, c.kind_b, c.kind_t = (_KIND[s.kind] for s in sides)
+        for s, segname, inname in zip(sides, ("seg_l", "seg_r", "seg_b", "seg_t"),
+                                      ("in_l", "in_r", "in_b", "in_t")):
+            seg = getattr(c, segname)
+            if s.kind == "inflow":
+                seg[0], seg[1] = float(s.segment[0]), float(s.segment[1])
+            iv = getattr(c, inname)
+            for m, v in enumerate(_inflow(s)):
+                iv[m] = v
+        self._cfg = c
+        self.dt_log = []
+
+    def _raise(self, what):
+        bad = np.argwhere(self.flags != 0)
+        i, j = (int(v) for v in bad[0])
+        raise OracleError(f"{what}; q = {self.q[i, j]}", step=self.step_count, cell=(i, j))
+
+    def max_rate(self):
+        L = lib()
+        self.flags[:] = 0
+        L.wbo_prepare_step(ctypes.byref(self._cfg), _p(self.q), _p(self.mask), _p(self.yfaces),
+                           _p(self.ycent), _p(self.y0s), _p(self.aeqs), _p(self.y0s_prev),
+                           _p(self.rhoE_c), _p(self.rhoE_fy), _p(self.col_rate),
+                           _p(self.flags))
+        rmax = float(self.col_rate.max())
+        if self.flags.any():
+            self._raise("non-admissible cell state")
+        if not np.isfinite(rmax) or rmax <= 0.0:
+            raise OracleError(f"non-finite wave speed (max rate {rmax})", step=self.step_count)
+        return rmax
+
+    def advance(self, max_dt=None):
+        L = lib()
+        g = self.grid
+        rmax = self.max_rate()
+        dt = self.cfl / rmax
+        if max_dt is not None and dt > max_dt:
+            dt = float(max_dt)
+        self.flags[:] = 0
+        cfg = ctypes.byref(self._cfg)
+        L.wbo_pass_reconstruct(cfg, _p(self.q), _p(self.mask), _p(self.aeqs), _p(self.rhoE_c),
+                               _p(self.rhoE_fy), _p(self.ycent), _p(self.yfaces),
+                               ctypes.c_double(0.5 * dt), _p(self.fW), _p(self.fE),
+                               _p(self.fS), _p(self.fN), _p(self.vol), _p(self.psi),
+                               _p(self.quiet), _p(self.flags))
+        if self.flags.any():
+            self._raise("non-admissible reconstructed face state")
+        L.wbo_sweep_vertical(cfg, _p(self.mask), _p(self.ycent), _p(self.fW), _p(self.fE),
+                             _p(self.DW), _p(self.DE), _p(self.y0s), _p(self.aeqs),
+                             _p(self.quiet))
+        L.wbo_sweep_horizontal(cfg, _p(self.mask), _p(self.xcent), _p(self.fS), _p(self.fN),
+                               _p(self.DS), _p(self.DN), _p(self.y0s), _p(self.aeqs),
+                               _p(self.quiet))
+        self.flags[:] = 0
+        L.wbo_apply_update(cfg, _p(self.q), _p(self.q_next), _p(self.mask), _p(self.fW),
+                           _p(self.fE), _p(self.fS), _p(self.fN), _p(self.DW), _p(self.DE),
+                           _p(self.DS), _p(self.DN), _p(self.vol),
+                           ctypes.c_double(dt / g.dx), ctypes.c_double(dt / g.dy),
+                           ctypes.c_double(dt / g.cell_area), _p(self.flags))
+        if self.flags.any():
+            self._raise("negative mass or volume fraction after update")
+        self.q, self.q_next = self.q_next, self.q
+        self.t += dt
+        self.step_count += 1
+        self.dt_log.append(dt)
+        return dt
+
+    def run_until(self, t_end, callback=None, max_steps=None):
+        tiny = 1.0e-12 * max(1.0, abs(t_end))
+        while self.t < t_end - tiny:
+            self.advance(max_dt=t_end - self.t)
+            if callback is not None:
+                callback(self)
+            if max_steps is not None and self.step_count >= max_steps:
+                break
+        return self.t
+
+    def run_steps(self, n):
+        for _ in range(n):
+            self.advance()
+
+
+def time_steps(sim, n):
+    """Wall time of n oracle steps (CPU baseline helper)."""
+    t0 = time.perf_counter()
+    sim.run_steps(n)
+    return time.perf_counter() - t0

@@ -1,0 +1,207 @@
+"""Deterministic scenario / initial-condition builders for the benchmark and
+parity configurations (the reference ships none --
+SPEC.md:554-659 describes them).
+
+Gravity initial conditions are *detection-consistent* (SURVEY.md App. A.9):
+alpha = 1-eps in the liquid and eps in the gas, the column surface level
+(y0_i, aeq_i) is detected exactly the way the solver does it
+(kernels.py:497-520, sequential sum in j), and the liquid density is
+aeq_i * eq_rho(y_j, y0_i) evaluated with libm exp, so that still liquid is
+bit-exactly quiet on the first step.
+"""
+
+from dataclasses import dataclass
+import math
+
+import numpy as np
+
+from .grid import BoundaryCondition, BoundarySpec, build_grid
+from .params import ModelParams
+from .state import eq_rho_profile
+
+__all__ = ["Scenario", "build_scenario", "detect_columns", "SCENARIOS",
+           "column_equilibrium_state"]
+
+
+@dataclass
+class Scenario:
+    name: str
+    grid: object
+    params: ModelParams
+    boundary: BoundarySpec
+    q0: np.ndarray          # (nx, ny, 5) conserved state, reference layout
+    t_end: float = None
+
+
+def detect_columns(alpha, mask, y_faces, dy):
+    """(y0s, aeqs) per column, identical to the solver's sequential detection
+    (kernels.py:432-453): numpy's add.accumulate is a strictly sequential sum,
+    and solid cells contribute an exact +0.0."""
+    fluid = mask != 0
+    a = np.where(fluid, alpha, 0.0)
+    ssum = np.cumsum(a, axis=1)[:, -1]
+    any_fluid = fluid.any(axis=1)
+    first = np.argmax(fluid, axis=1)
+    ylow = np.where(any_fluid, np.asarray(y_faces)[first], y_faces[0])
+    aeq = np.where(any_fluid, alpha[np.arange(alpha.shape[0]), first], 1.0)
+    return ylow + ssum * dy, aeq
+
+
+def column_equilibrium_state(grid, params, alpha, u=None, v=None, gas_rho=None):
+    """Conserved state for a volume-fraction field: liquid density follows
+    each column's detected equilibrium aeq*eq_rho(y, y0); gas (alpha <= 10 eps
+    when ``gas_rho`` is given) gets rho = gas_rho."""
+    nx, ny = grid.nx, grid.ny
+    yc = grid.y_centers
+    y0s, aeqs = detect_columns(alpha, grid.mask, grid.y_faces, grid.dy)
+    rho_a = np.empty((nx, ny))
+    # one libm-exp profile per distinct surface level (few in practice)
+    for y0 in np.unique(y0s):
+        cols = y0s == y0
+        rho_a[cols] = eq_rho_profile(yc, y0, params)[None, :]
+    arho = aeqs[:, None] * rho_a
+    if gas_rho is not None:
+        gas = alpha <= 10.0 * params.epsilon
+        arho = np.where(gas, alpha * gas_rho, arho)
+    q = np.zeros((nx, ny, 5))
+    q[..., 0] = arho
+    if u is not None:
+        q[..., 1] = arho * u
+    if v is not None:
+        q[..., 2] = arho * v
+    q[..., 3] = alpha
+    q[..., 4] = yc[None, :]
+    return q
+
+
+def _centres(grid):
+    return np.meshgrid(grid.x_centers, grid.y_centers, indexing="ij")
+
+
+def _box(x, y, x0, x1, y0, y1):
+    return (x >= x0) & (x <= x1) & (y >= y0) & (y <= y1)
+
+
+def _dambreak(grid, params, region, gas_rho=None):
+    eps = params.epsilon
+    x, y = _centres(grid)
+    liquid = _box(x, y, *region)
+    alpha = np.where(liquid, 1.0 - eps, eps)
+    return column_equilibrium_state(grid, params, alpha,
+                                    gas_rho=params.rho0 if gas_rho is None else gas_rho)
+
+
+def _lake(name, res, obstacles, perturb_seed=None):
+    params = ModelParams(k0=2.78e5)
+    grid = build_grid((-0.5, 0.5, 0.0, 1.0), res, obstacles)
+    alpha = np.ones((grid.nx, grid.ny))
+    q = column_equilibrium_state(grid, params, alpha)
+    if perturb_seed is not None:
+        rng = np.random.default_rng(perturb_seed)
+        kx, ky = rng.integers(1, 4, size=2)
+        phi = rng.uniform(0.0, 2.0 * math.pi)
+        x, y = _centres(grid)
+        rho = q[..., 0] * (1.0 + 1e-3 * np.sin(2 * math.pi * kx * x + phi)
+                           * np.cos(2 * math.pi * ky * y))
+        u = 1e-2 * np.cos(2 * math.pi * ky * y)
+        v = 1e-2 * np.sin(2 * math.pi * kx * x)
+        q[..., 0] = rho
+        q[..., 1] = rho * u
+        q[..., 2] = rho * v
+    return Scenario(name, grid, params, BoundarySpec(), q)
+
+
+LAKE_OBSTACLES = ((-0.25, 0.25, 0.0, 0.33), (0.30, 0.40, 0.0, 0.60),
+                  (-0.45, -0.35, 0.0, 0.17))
+
+
+def build_scenario(name, resolution=None, seed=0):
+    """Build one named configuration.
+
+    * ``dambreak-dry``  -- C1, [-50,50]x[0,4], liquid [-50,0]x[0,1.4618], k0 6.37e5
+      (PAPER.md:1089-1094); reflective L/R/bottom, transmissive top.
+    * ``lake``          -- C2, lake at rest with alpha = 1 over three bottom
+      obstacles, k0 2.78e5 (PAPER.md:849-851 plus two survey obstacles).
+    * ``equilibrium-obstacle`` -- the paper's single-obstacle lake.
+    * ``perturbed-lake`` -- C2 geometry with a seeded smooth perturbation.
+    * ``drop``          -- C3, [-3,3]^2, g = 0, k0 2.25e9, u = (-100x, 100y) in r<1.
+    * ``weir``          -- C4, [-7.5,7.5]x[0,2.1], strip [0,dx]x[0,0.7], liquid
+      [-7.5,0]x[0,1.5], k0 6.54e5.
+    * ``wall-impact``   -- C5, [0,3.2]x[0,1.8], liquid [0,1.2]x[0,0.6], k0 2.62e5,
+      transmissive top.
+    * ``jet``           -- small inflow case (inflow segment on the left side,
+      transmissive right/top) that exercises the inflow ghost.
+    * ``tait7``         -- a gamma = 7 dambreak (pow() path; parity by tolerance).
+    """
+    if name == "dambreak-dry":
+        res = resolution or (200, 100)
+        params = ModelParams(k0=6.37e5)
+        grid = build_grid((-50.0, 50.0, 0.0, 4.0), res)
+        q = _dambreak(grid, params, (-50.0, 0.0, 0.0, 1.4618))
+        bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
+        return Scenario(name, grid, params, bnd, q)
+    if name == "lake":
+        return _lake(name, resolution or (2048, 1024), LAKE_OBSTACLES)
+    if name == "equilibrium-obstacle":
+        return _lake(name, resolution or (100, 100), LAKE_OBSTACLES[:1])
+    if name == "perturbed-lake":
+        return _lake(name, resolution or (128, 128), LAKE_OBSTACLES, perturb_seed=seed)
+    if name == "drop":
+        res = resolution or (4096, 4096)
+        params = ModelParams(k0=2.25e9, g=0.0)
+        grid = build_grid((-3.0, 3.0, -3.0, 3.0), res)
+        x, y = _centres(grid)
+        inside = x * x + y * y <= 1.0
+        eps = params.epsilon
+        alpha = np.where(inside, 1.0 - eps, eps)
+        rho = params.rho0
+        q = np.zeros((grid.nx, grid.ny, 5))
+        q[..., 0] = alpha * rho
+        q[..., 1] = np.where(inside, q[..., 0] * (-100.0 * x), 0.0)
+        q[..., 2] = np.where(inside, q[..., 0] * (100.0 * y), 0.0)
+        q[..., 3] = alpha
+        q[..., 4] = grid.y_centers[None, :]
+        return Scenario(name, grid, params, BoundarySpec(), q)
+    if name == "weir":
+        res = resolution or (16384, 8192)
+        params = ModelParams(k0=6.54e5)
+        dx = 15.0 / res[0]
+        grid = build_grid((-7.5, 7.5, 0.0, 2.1), res, [(0.0, dx, 0.0, 0.7)])
+        q = _dambreak(grid, params, (-7.5, 0.0, 0.0, 1.5))
+        return Scenario(name, grid, params, BoundarySpec(), q)
+    if name == "wall-impact":
+        res = resolution or (32768, 16384)
+        params = ModelParams(k0=2.62e5)
+        grid = build_grid((0.0, 3.2, 0.0, 1.8), res)
+        q = _dambreak(grid, params, (0.0, 1.2, 0.0, 0.6))
+        bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
+        return Scenario(name, grid, params, bnd, q)
+    if name == "jet":
+        res = resolution or (96, 64)
+        params = ModelParams(k0=2.78e5, g=9.81)
+        grid = build_grid((0.0, 3.0, 0.0, 2.0), res, [(1.8, 2.1, 0.0, 0.9)])
+        q = _dambreak(grid, params, (0.0, 0.6, 0.0, 0.5))
+        eps = params.epsilon
+        state = (params.rho0, 2.0, 0.0, 1.0 - eps, 0.0)
+        bnd = BoundarySpec(left=BoundaryCondition("inflow", state, (0.2, 0.6)),
+                           right=BoundaryCondition("transmissive"),
+                           top=BoundaryCondition("transmissive"))
+        return Scenario(name, grid, params, bnd, q)
+    if name == "tait7":
+        res = resolution or (64, 32)
+        params = ModelParams(k0=3.0e5, gamma=7.0)
+        grid = build_grid((-4.0, 4.0, 0.0, 2.0), res)
+        eps = params.epsilon
+        x, y = _centres(grid)
+        alpha = np.where(_box(x, y, -4.0, 0.0, 0.0, 1.0), 1.0 - eps, eps)
+        rho = params.rho0
+        q = np.zeros((grid.nx, grid.ny, 5))
+        q[..., 0] = alpha * rho
+        q[..., 3] = alpha
+        q[..., 4] = grid.y_centers[None, :]
+        return Scenario(name, grid, params, BoundarySpec(), q)
+    raise ValueError(f"unknown scenario {name!r}")
+
+
+SCENARIOS = ("dambreak-dry", "lake", "equilibrium-obstacle", "perturbed-lake", "drop",
+             "weir", "wall-impact", "jet", "tait7")
