@@ -1,0 +1,143 @@
+/*
+ * wbflow_b200.h -- C ABI of the B200-native time-stepping hot path.
+ *
+ * Drop-in boundary: the reference (pkg/src/wbflow, Python + Numba) has no
+ * native FFI of its own; its hot-path boundary is the Python driver API in
+ * timestepper.py and the Numba kernel entry points in kernels.py.  Each entry
+ * point below names the reference interface it replaces.  Conventions:
+ * plain C types only, int return status (WB_OK = 0), one opaque handle per
+ * simulation (or per x-slab for multi-GPU), all device work stream-ordered on
+ * the handle's stream, not thread-safe per handle.  State arrays crossing the
+ * boundary use the reference layout (i, j, m) with m fastest and 5
+ * components (a*rho, a*rho*u, a*rho*v, alpha, y).
+ */
+#ifndef WBFLOW_B200_H
+#define WBFLOW_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WB_OK 0
+#define WB_E_ARG -1       /* invalid argument / configuration */
+#define WB_E_CUDA -2      /* CUDA runtime failure */
+#define WB_E_HEIGHT -3    /* q[...,4] != y_centers for a fluid cell */
+#define WB_E_STATE -4     /* no state uploaded */
+
+/* numerical error codes reported in wb_error.code (timestepper.py:154-158,
+ * 181-182, 205-207) */
+#define WB_ERR_NONE 0
+#define WB_ERR_CELL_STATE 1   /* "non-admissible cell state" */
+#define WB_ERR_WAVE_SPEED 2   /* "non-finite wave speed (max rate ...)" */
+#define WB_ERR_FACE 3         /* "non-admissible reconstructed face state" */
+#define WB_ERR_MASS 4         /* "negative mass or volume fraction after update" */
+
+typedef struct wb_handle wb_handle;
+
+typedef struct {
+  int32_t nx, ny;            /* global grid (grid.py:21-38) */
+  int32_t i_begin, i_end;    /* owned global columns [i_begin, i_end) (x-slab) */
+  double dx, dy;
+  double k0, rho0, gamma, g, epsilon; /* params.py:6-21 */
+  double cfl;                /* timestepper.py:51 */
+  int32_t bc_kind[4];        /* left,right,bottom,top: 1 reflective 2 transmissive 3 inflow */
+  double inflow_seg[4][2];   /* grid.py:110-123 segment per side */
+  double inflow_q[4][4];     /* conserved inflow state (timestepper.py:33-37) */
+  int32_t device;            /* CUDA device ordinal */
+  int32_t rows_per_block;    /* 0 = auto */
+} wb_config;
+
+typedef struct {
+  int32_t code;              /* WB_ERR_* */
+  int64_t step;              /* committed steps when the error happened */
+  int32_t i, j;              /* first failing cell in i-major order, -1 if none */
+  double rmax;               /* the offending rate for WB_ERR_WAVE_SPEED */
+} wb_error;
+
+typedef struct {
+  double t, dt, rmax;
+  int64_t step;
+  int32_t stop;              /* 0 running, >0 error code, -1 target reached */
+  int32_t cur;
+  uint64_t n_second_order, x_faces_solved, y_faces_solved; /* last step */
+} wb_status;
+
+/* Simulation.__init__ (timestepper.py:51-103): grid, params, boundary and
+ * per-face BC classification.  mask is the global (nx, ny) uint8 array
+ * (grid.py:35); xcent/ycent/yfaces are grid.x_centers/y_centers/y_faces
+ * (grid.py:40-54), passed so the device uses the reference's exact doubles. */
+int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
+              const double* ycent, const double* yfaces, wb_handle** out);
+int wb_destroy(wb_handle* h);
+/* run all work on this CUDA stream (e.g. torch.cuda.current_stream()) */
+int wb_set_stream(wb_handle* h, void* cuda_stream);
+
+/* Simulation.q assignment (timestepper.py:64-69): q holds n_cols columns
+ * starting at global column i_first, (n_cols, ny, 5); it must cover the owned
+ * columns plus the 2-column halo that exists in the domain.  is_device != 0
+ * means q is a device pointer.  On WB_E_HEIGHT, *bad_i / *bad_j name the cell. */
+int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
+                 int32_t is_device, int32_t* bad_i, int32_t* bad_j);
+/* Simulation.q read (owned columns, (i_end-i_begin, ny, 5)); solid cells come
+ * back with the values uploaded for them and q[...,4] = y_centers. */
+int wb_get_state(wb_handle* h, double* q, int32_t is_device);
+/* which = 0: current state (Simulation.q), 1: the other buffer (Simulation.q_next) */
+int wb_get_state_buf(wb_handle* h, double* q, int32_t which, int32_t is_device);
+/* one cell of the current state (error messages) */
+int wb_get_cell(wb_handle* h, int32_t i, int32_t j, double* q5);
+
+/* Simulation.max_rate / compute_dt (timestepper.py:143-159, 232-237):
+ * detection + admissibility + CFL rate max of the current state */
+int wb_max_rate(wb_handle* h, double* rmax, wb_error* err);
+/* Simulation.detect (timestepper.py:132-135): per-column (y0, aeq), owned */
+int wb_get_columns(wb_handle* h, double* y0s, double* aeqs);
+
+/* Simulation.advance (timestepper.py:163-218): one step; max_dt = NaN for
+ * none.  On a numerical error the step is not committed (t, step and the
+ * state stay at step n) and err->code != 0. */
+int wb_advance(wb_handle* h, double max_dt, double* dt_out, wb_error* err);
+/* Simulation.run_until (timestepper.py:220-229) without callback, as a
+ * device-side loop: t_end = NaN for "no time limit", max_steps < 0 for none,
+ * chunk = steps enqueued between host checks (captured in a CUDA graph). */
+int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_error* err);
+int wb_get_status(wb_handle* h, wb_status* s);
+int wb_set_time(wb_handle* h, double t, int64_t step);
+/* per-step dt log written by the device (first `cap` steps) */
+int wb_get_dt_log(wb_handle* h, double* out, int64_t n);
+
+/* Stage arrays of one step (the reference's fW,fE,fS,fN,vol,psi,quiet,
+ * DW,DE,DS,DN, rhoE_c, rhoE_fy work arrays, timestepper.py:82-95): runs the
+ * same fused kernel with debug stores enabled; arrays are host pointers in
+ * the reference layout for the owned columns (any may be NULL). */
+typedef struct {
+  double *fW, *fE, *fS, *fN, *vol, *psi, *DW, *DE, *DS, *DN, *rhoE_c, *rhoE_fy;
+  uint8_t* quiet;
+} wb_stage_arrays;
+int wb_advance_debug(wb_handle* h, double max_dt, double* dt_out, wb_error* err,
+                     const wb_stage_arrays* out);
+
+/* ---- x-slab multi-GPU building blocks (driven by the host over NCCL) ---- */
+/* device address of the 2 x uint64 reduction vector [~errkey, rmax_bits]
+ * (MAX-allreduce across ranks between wb_step_local and wb_finalize) */
+int wb_reduce_ptr(wb_handle* h, void** dev_ptr);
+/* device address of the current-state rate slot (uint64 bits, MAX) and of
+ * the prepare-error key slot (uint64, MIN) used once after an upload */
+int wb_prepare_ptrs(wb_handle* h, void** rmax_bits, void** key_prep);
+int wb_prepare_local(wb_handle* h);         /* enqueue detect + prepare (no sync) */
+int wb_check_prepare(wb_handle* h, double* rmax, wb_error* err); /* sync + read */
+int wb_step_local(wb_handle* h, double max_dt, double t_end, int32_t mode);
+int wb_finalize(wb_handle* h);
+/* halo columns: 2 x 4 x 2 x ny doubles (side, component, column, j) */
+int wb_halo_count(wb_handle* h, int64_t* n_doubles);
+int wb_pack_halo(wb_handle* h, void* send_dev);
+int wb_unpack_halo(wb_handle* h, const void* recv_dev, int32_t have_left, int32_t have_right);
+int wb_sync(wb_handle* h);
+
+const char* wb_last_error(void);
+int wb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

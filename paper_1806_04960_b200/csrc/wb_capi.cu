@@ -1,0 +1,720 @@
+// wb_capi.cu -- extern "C" boundary of the B200 hot path (include/wbflow_b200.h).
+//
+// Host-side runtime: owns the device buffers of one simulation slab, launches
+// the step pipeline (detect -> fused step -> finalize) on its own stream,
+// captures multi-step chunks in a CUDA graph for device-side run loops, and
+// translates device status into the reference's error contract.  No torch
+// types cross this boundary.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include <string>
+#include "../../include/wbflow_b200.h"
+#include "wb_kernels.cuh"
+#include "wb_step.cu"  // single translation unit: kernels + c_exp_tab
+
+
+using namespace wb;
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                     \
+  do {                                                                            \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess) {                                                      \
+      g_err = std::string(#x) + ": " + cudaGetErrorString(e_);                    \
+      return WB_E_CUDA;                                                           \
+    }                                                                             \
+  } while (0)
+
+namespace {
+constexpr int NT = 64;
+constexpr long long DTLOG_CAP = 1 << 20;
+
+// small kernel that sets the run parameters in the device status
+__global__ void k_set_run(Status* st, int mode, int has_max_dt, double max_dt, double t_end,
+                          double tiny, long long max_steps, int reset_stop) {
+  st->mode = mode;
+  st->has_max_dt = has_max_dt;
+  st->max_dt = max_dt;
+  st->t_end = t_end;
+  st->tiny = tiny;
+  st->max_steps = max_steps;
+  if (reset_stop) st->stop = 0;
+}
+__global__ void k_reset_state(Status* st, double t, long long step) {
+  st->rmax_bits = 0ull;
+  st->rmax_next_bits = 0ull;
+  st->key_recon = KEY_NONE;
+  st->key_update = KEY_NONE;
+  st->key_prep = KEY_NONE;
+  st->cur = 0;
+  st->stop = 0;
+  st->t = t;
+  st->step = step;
+  st->dt = 0.0;
+  st->max_steps = -1;
+  st->mode = 0;
+  st->has_max_dt = 0;
+  st->err_code = 0;
+  st->rmax_used_bits = 0ull;
+}
+__global__ void k_begin_prepare(Status* st) {
+  st->rmax_bits = 0ull;
+  st->key_prep = KEY_NONE;
+  st->stop = 0;
+}
+__global__ void k_set_time(Status* st, double t, long long step) {
+  st->t = t;
+  st->step = step;
+}
+}  // namespace
+
+struct wb_handle {
+  Geo G;
+  Phys P;
+  Bufs B;
+  int dev = 0;
+  bool g1 = true;
+  int L = 64;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double* planes = nullptr;
+  uint8_t* mask = nullptr;
+  double *y0s = nullptr, *aeqs = nullptr, *ycent = nullptr, *yfaces = nullptr,
+         *xcent = nullptr;
+  Status* st = nullptr;
+  Status* h_st = nullptr;
+  double* dtlog = nullptr;
+  unsigned long long* scratch = nullptr;  // [0] bad-height key
+  double* tmp = nullptr;                  // AoS staging
+  size_t tmp_bytes = 0;
+  bool have_state = false;
+  bool need_prepare = true;
+  double t = 0.0;
+  long long step = 0;
+  cudaGraphExec_t graph = nullptr;
+  int graph_chunk = 0;
+  dim3 grid_step;
+};
+
+static int ensure_tmp(wb_handle* h, size_t bytes) {
+  if (h->tmp_bytes >= bytes) return WB_OK;
+  if (h->tmp) cudaFree(h->tmp);
+  h->tmp = nullptr;
+  h->tmp_bytes = 0;
+  CK(cudaMalloc(&h->tmp, bytes));
+  h->tmp_bytes = bytes;
+  return WB_OK;
+}
+
+static int read_status(wb_handle* h) {
+  CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(Status), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->t = h->h_st->t;
+  h->step = h->h_st->step;
+  return WB_OK;
+}
+
+static void fill_error(wb_handle* h, wb_error* err) {
+  if (!err) return;
+  const Status& s = *h->h_st;
+  err->code = s.stop > 0 ? s.err_code : WB_ERR_NONE;
+  err->step = s.err_step;
+  err->i = -1;
+  err->j = -1;
+  err->rmax = s.err_rmax;
+  if (s.stop > 0 && s.err_key >= 0) {
+    err->i = (int32_t)(s.err_key / h->G.ny);
+    err->j = (int32_t)(s.err_key % h->G.ny);
+  }
+}
+
+template <bool DEBUG>
+static void launch_step(wb_handle* h, const Dbg& D) {
+  if (h->g1)
+    k_step<NT, true, DEBUG><<<h->grid_step, NT, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+  else
+    k_step<NT, false, DEBUG><<<h->grid_step, NT, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+}
+
+static void launch_detect(wb_handle* h) {
+  k_detect<<<(h->G.ncol + 127) / 128, 128, 0, h->stream>>>(h->G, h->B, h->P.dy);
+}
+
+static void enqueue_step(wb_handle* h) {
+  launch_detect(h);
+  k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
+  launch_step<false>(h, Dbg{});
+  k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
+  k_finalize<<<1, 1, 0, h->stream>>>(h->st, h->G.cfl, h->dtlog, DTLOG_CAP);
+}
+
+// detect + admissibility/rate of the current state; sets code 1 / 2 errors
+static int do_prepare(wb_handle* h, double* rmax, wb_error* err) {
+  k_begin_prepare<<<1, 1, 0, h->stream>>>(h->st);
+  launch_detect(h);
+  if (h->g1)
+    k_prepare<true><<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P);
+  else
+    k_prepare<false><<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P);
+  CK(cudaGetLastError());
+  int rc = read_status(h);
+  if (rc) return rc;
+  Status& s = *h->h_st;
+  double r = 0.0;
+  unsigned long long b = s.rmax_bits;
+  memcpy(&r, &b, 8);
+  if (rmax) *rmax = r;
+  if (err) {
+    err->code = WB_ERR_NONE;
+    err->i = err->j = -1;
+    err->step = s.step;
+    err->rmax = r;
+    if (s.key_prep != KEY_NONE) {
+      err->code = WB_ERR_CELL_STATE;
+      err->i = (int32_t)(s.key_prep / h->G.ny);
+      err->j = (int32_t)(s.key_prep % h->G.ny);
+    } else if (!(isfinite(r) && r > 0.0)) {
+      err->code = WB_ERR_WAVE_SPEED;
+    }
+  }
+  return WB_OK;
+}
+
+extern "C" {
+
+const char* wb_last_error(void) { return g_err.c_str(); }
+int wb_version(void) { return 1; }
+
+int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
+              const double* ycent, const double* yfaces, wb_handle** out) {
+  if (!cfg || !mask || !xcent || !ycent || !yfaces || !out) return WB_E_ARG;
+  if (cfg->nx < 2 || cfg->ny < 2 || cfg->i_begin < 0 || cfg->i_end > cfg->nx ||
+      cfg->i_end <= cfg->i_begin || !(cfg->cfl > 0.0 && cfg->cfl < 1.0)) {
+    g_err = "invalid wb_config";
+    return WB_E_ARG;
+  }
+  wb_handle* h = new wb_handle();
+  h->dev = cfg->device;
+  CK(cudaSetDevice(h->dev));
+  static bool tab_done[64] = {false};
+  if (h->dev < 64 && !tab_done[h->dev]) {
+    CK(cudaMemcpyToSymbol(c_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
+    tab_done[h->dev] = true;
+  }
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+
+  Geo& G = h->G;
+  memset(&G, 0, sizeof(G));
+  G.nx = cfg->nx;
+  G.ny = cfg->ny;
+  G.i_begin = cfg->i_begin;
+  G.nxl = cfg->i_end - cfg->i_begin;
+  G.ncol = G.nxl + 2 * HALO;
+  G.pitch = (G.ncol + 31) / 32 * 32;
+  for (int s = 0; s < 4; s++) {
+    G.kind[s] = cfg->bc_kind[s];
+    G.seg[s][0] = cfg->inflow_seg[s][0];
+    G.seg[s][1] = cfg->inflow_seg[s][1];
+    for (int m = 0; m < 4; m++) G.inflow[s][m] = cfg->inflow_q[s][m];
+  }
+  // reconstruction ghost codes: reflective -> 1, everything else -> 2
+  // (timestepper.py:98-101)
+  G.bcw = cfg->bc_kind[0] == BC_REFL ? BC_REFL : BC_TRANS;
+  G.bce = cfg->bc_kind[1] == BC_REFL ? BC_REFL : BC_TRANS;
+  G.bcs = cfg->bc_kind[2] == BC_REFL ? BC_REFL : BC_TRANS;
+  G.bcn = cfg->bc_kind[3] == BC_REFL ? BC_REFL : BC_TRANS;
+  G.cfl = cfg->cfl;
+
+  Phys& P = h->P;
+  P.k0 = cfg->k0;
+  P.rho0 = cfg->rho0;
+  P.gamma = cfg->gamma;
+  P.g = cfg->g;
+  P.eps = cfg->epsilon;
+  P.c2ref = cfg->k0 / cfg->rho0;
+  P.cref = sqrt(P.c2ref);
+  P.grk = cfg->g * cfg->rho0 / cfg->k0;
+  P.neg_grk = -P.grk;
+  P.athr = 10.0 * cfg->epsilon;
+  P.dx = cfg->dx;
+  P.dy = cfg->dy;
+  P.hx = 0.5 * cfg->dx;
+  P.hy = 0.5 * cfg->dy;
+  P.rdx2 = 1.0 / (2.0 * cfg->dx);
+  P.rdy2 = 1.0 / (2.0 * cfg->dy);
+  P.area = cfg->dx * cfg->dy;
+  P.rho_lo = 0.5 * cfg->rho0;
+  P.rho_hi = 2.0 * cfg->rho0;
+  // vmax = 2 sqrt(sound_c2(rho0)) (kernels.py:1237); sound_c2(rho0) for any
+  // gamma is gamma*k0/rho0*(1)^(gamma-1)
+  double c2r = cfg->gamma == 1.0 ? cfg->k0 / cfg->rho0
+                                 : cfg->gamma * cfg->k0 / cfg->rho0 * pow(1.0, cfg->gamma - 1.0);
+  P.vmax = 2.0 * sqrt(c2r);
+  h->g1 = cfg->gamma == 1.0;
+
+  const size_t plane = (size_t)G.pitch * G.ny;
+  CK(cudaMalloc(&h->planes, 8 * plane * sizeof(double)));
+  CK(cudaMemsetAsync(h->planes, 0, 8 * plane * sizeof(double), h->stream));
+  for (int b = 0; b < 2; b++)
+    for (int m = 0; m < 4; m++) h->B.q[b][m] = h->planes + (b * 4 + m) * plane;
+  // mask in device layout (j, stored column), zero outside the domain
+  {
+    uint8_t* hm = (uint8_t*)calloc(plane, 1);
+    for (int c = 0; c < G.ncol; c++) {
+      int gi = G.i_begin + c - HALO;
+      if (gi < 0 || gi >= G.nx) continue;
+      for (int j = 0; j < G.ny; j++) hm[(size_t)j * G.pitch + c] = mask[(size_t)gi * G.ny + j];
+    }
+    CK(cudaMalloc(&h->mask, plane));
+    cudaError_t e = cudaMemcpy(h->mask, hm, plane, cudaMemcpyHostToDevice);
+    free(hm);
+    CK(e);
+  }
+  CK(cudaMalloc(&h->y0s, G.pitch * sizeof(double)));
+  CK(cudaMalloc(&h->aeqs, G.pitch * sizeof(double)));
+  CK(cudaMemset(h->y0s, 0, G.pitch * sizeof(double)));
+  CK(cudaMemset(h->aeqs, 0, G.pitch * sizeof(double)));
+  CK(cudaMalloc(&h->ycent, G.ny * sizeof(double)));
+  CK(cudaMalloc(&h->yfaces, (G.ny + 1) * sizeof(double)));
+  CK(cudaMemcpy(h->ycent, ycent, G.ny * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->yfaces, yfaces, (G.ny + 1) * sizeof(double), cudaMemcpyHostToDevice));
+  {
+    double* hx = (double*)calloc(G.pitch, sizeof(double));
+    for (int c = 0; c < G.ncol; c++) {
+      int gi = G.i_begin + c - HALO;
+      if (gi >= 0 && gi < G.nx) hx[c] = xcent[gi];
+    }
+    CK(cudaMalloc(&h->xcent, G.pitch * sizeof(double)));
+    cudaError_t e = cudaMemcpy(h->xcent, hx, G.pitch * sizeof(double), cudaMemcpyHostToDevice);
+    free(hx);
+    CK(e);
+  }
+  CK(cudaMalloc(&h->st, sizeof(Status)));
+  CK(cudaHostAlloc(&h->h_st, sizeof(Status), cudaHostAllocDefault));
+  CK(cudaMalloc(&h->dtlog, DTLOG_CAP * sizeof(double)));
+  CK(cudaMalloc(&h->scratch, 4 * sizeof(unsigned long long)));
+  k_reset_state<<<1, 1, 0, h->stream>>>(h->st, 0.0, 0);
+  CK(cudaGetLastError());
+
+  Bufs& B = h->B;
+  B.mask = h->mask;
+  B.y0s = h->y0s;
+  B.aeqs = h->aeqs;
+  B.ycent = h->ycent;
+  B.yfaces = h->yfaces;
+  B.xcent = h->xcent;
+  B.st = h->st;
+  B.dtlog = h->dtlog;
+  B.dtlog_cap = DTLOG_CAP;
+
+  int L = cfg->rows_per_block > 0 ? cfg->rows_per_block : 64;
+  // keep at least ~4 CTAs per SM on small grids
+  int bx = (G.nxl + NT - 2 * HALO - 1) / (NT - 2 * HALO);
+  while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
+  h->L = L;
+  h->grid_step = dim3(bx, (G.ny + L - 1) / L);
+  CK(cudaStreamSynchronize(h->stream));
+  *out = h;
+  return WB_OK;
+}
+
+int wb_destroy(wb_handle* h) {
+  if (!h) return WB_OK;
+  cudaSetDevice(h->dev);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  cudaFree(h->planes);
+  cudaFree(h->mask);
+  cudaFree(h->y0s);
+  cudaFree(h->aeqs);
+  cudaFree(h->ycent);
+  cudaFree(h->yfaces);
+  cudaFree(h->xcent);
+  cudaFree(h->st);
+  cudaFreeHost(h->h_st);
+  cudaFree(h->dtlog);
+  cudaFree(h->scratch);
+  if (h->tmp) cudaFree(h->tmp);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return WB_OK;
+}
+
+int wb_set_stream(wb_handle* h, void* s) {
+  if (!h) return WB_E_ARG;
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  h->stream = (cudaStream_t)s;
+  h->own_stream = false;
+  if (h->graph) {
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  return WB_OK;
+}
+
+int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
+                 int32_t is_device, int32_t* bad_i, int32_t* bad_j) {
+  if (!h || !q || n_cols <= 0) return WB_E_ARG;
+  const Geo& G = h->G;
+  int need_lo = std::max(0, G.i_begin - HALO);
+  int need_hi = std::min(G.nx, G.i_begin + G.nxl + HALO);
+  if (i_first > need_lo || i_first + n_cols < need_hi) {
+    g_err = "wb_set_state: q does not cover the owned columns plus halo";
+    return WB_E_ARG;
+  }
+  CK(cudaSetDevice(h->dev));
+  const size_t bytes = (size_t)n_cols * G.ny * 5 * sizeof(double);
+  const double* src = q;
+  if (!is_device) {
+    int rc = ensure_tmp(h, bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(h->tmp, q, bytes, cudaMemcpyHostToDevice, h->stream));
+    src = h->tmp;
+  }
+  CK(cudaMemsetAsync(h->scratch, 0xff, sizeof(unsigned long long), h->stream));
+  k_aos_to_planes<<<148 * 8, 256, 0, h->stream>>>(h->G, h->B, src, i_first, n_cols, h->scratch);
+  CK(cudaGetLastError());
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, h->scratch, 8, cudaMemcpyDeviceToHost, h->stream));
+  k_reset_state<<<1, 1, 0, h->stream>>>(h->st, h->t, h->step);
+  CK(cudaStreamSynchronize(h->stream));
+  h->need_prepare = true;
+  if (bad != KEY_NONE) {
+    if (bad_i) *bad_i = (int32_t)(bad / G.ny);
+    if (bad_j) *bad_j = (int32_t)(bad % G.ny);
+    h->have_state = false;
+    g_err = "q[..., 4] must equal grid.y_centers for fluid cells";
+    return WB_E_HEIGHT;
+  }
+  h->have_state = true;
+  return WB_OK;
+}
+
+int wb_get_state(wb_handle* h, double* q, int32_t is_device) {
+  return wb_get_state_buf(h, q, 0, is_device);
+}
+
+int wb_get_state_buf(wb_handle* h, double* q, int32_t which, int32_t is_device) {
+  if (!h || !q) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  const size_t bytes = (size_t)h->G.nxl * h->G.ny * 5 * sizeof(double);
+  double* dst = q;
+  if (!is_device) {
+    int rc = ensure_tmp(h, bytes);
+    if (rc) return rc;
+    dst = h->tmp;
+  }
+  k_planes_to_aos<<<148 * 8, 256, 0, h->stream>>>(h->G, h->B, dst, which ? 1 : -1);
+  CK(cudaGetLastError());
+  if (!is_device) CK(cudaMemcpyAsync(q, dst, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return WB_OK;
+}
+
+int wb_get_cell(wb_handle* h, int32_t i, int32_t j, double* q5) {
+  if (!h || !q5) return WB_E_ARG;
+  int c = i - h->G.i_begin + HALO;
+  if (c < 0 || c >= h->G.ncol || j < 0 || j >= h->G.ny) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  int rc = read_status(h);
+  if (rc) return rc;
+  int cur = h->h_st->cur;
+  size_t o = (size_t)j * h->G.pitch + c;
+  for (int m = 0; m < 4; m++)
+    CK(cudaMemcpy(q5 + m, h->B.q[cur][m] + o, sizeof(double), cudaMemcpyDeviceToHost));
+  double y;
+  CK(cudaMemcpy(&y, h->ycent + j, sizeof(double), cudaMemcpyDeviceToHost));
+  q5[4] = y;
+  return WB_OK;
+}
+
+int wb_max_rate(wb_handle* h, double* rmax, wb_error* err) {
+  if (!h) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  int rc = do_prepare(h, rmax, err);
+  if (rc) return rc;
+  h->need_prepare = err ? err->code != WB_ERR_NONE : false;
+  return WB_OK;
+}
+
+int wb_get_columns(wb_handle* h, double* y0s, double* aeqs) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamSynchronize(h->stream));
+  if (y0s)
+    CK(cudaMemcpy(y0s, h->y0s + HALO, h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost));
+  if (aeqs)
+    CK(cudaMemcpy(aeqs, h->aeqs + HALO, h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost));
+  return WB_OK;
+}
+
+static int advance_impl(wb_handle* h, double max_dt, double* dt_out, wb_error* err,
+                        const Dbg* dbg) {
+  if (!h) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  if (err) err->code = WB_ERR_NONE;
+  if (h->need_prepare) {
+    wb_error e{};
+    int rc = do_prepare(h, nullptr, &e);
+    if (rc) return rc;
+    if (e.code != WB_ERR_NONE) {
+      if (err) *err = e;
+      return WB_OK;
+    }
+    h->need_prepare = false;
+  }
+  int has = !isnan(max_dt);
+  k_set_run<<<1, 1, 0, h->stream>>>(h->st, 0, has, has ? max_dt : 0.0, 0.0, 0.0,
+                                     h->step + 1, 1);
+  launch_detect(h);  // after k_set_run: detection skips when the run is stopped
+  k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
+  if (dbg)
+    launch_step<true>(h, *dbg);
+  else
+    launch_step<false>(h, Dbg{});
+  k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
+  k_finalize<<<1, 1, 0, h->stream>>>(h->st, h->G.cfl, h->dtlog, DTLOG_CAP);
+  CK(cudaGetLastError());
+  int rc = read_status(h);
+  if (rc) return rc;
+  fill_error(h, err);
+  if (h->h_st->stop > 0) h->need_prepare = true;  // a failed step leaves q^n current
+  if (dt_out) *dt_out = h->h_st->dt;
+  return WB_OK;
+}
+
+int wb_advance(wb_handle* h, double max_dt, double* dt_out, wb_error* err) {
+  return advance_impl(h, max_dt, dt_out, err, nullptr);
+}
+
+int wb_advance_debug(wb_handle* h, double max_dt, double* dt_out, wb_error* err,
+                     const wb_stage_arrays* out) {
+  if (!h || !out) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  const size_t n = (size_t)h->G.nxl * h->G.ny;
+  const size_t b5 = n * 5 * sizeof(double);
+  double* base = nullptr;
+  uint8_t* qd = nullptr;
+  CK(cudaMalloc(&base, 10 * b5));
+  CK(cudaMemset(base, 0, 10 * b5));
+  CK(cudaMalloc(&qd, n));
+  CK(cudaMemset(qd, 0, n));
+  Dbg D;
+  double** slots[10] = {&D.fW, &D.fE, &D.fS, &D.fN, &D.vol, &D.psi, &D.DW, &D.DE, &D.DS, &D.DN};
+  for (int k = 0; k < 10; k++) *slots[k] = base + k * n * 5;
+  D.quiet = qd;
+  int rc = advance_impl(h, max_dt, dt_out, err, &D);
+  if (rc == WB_OK) {
+    double* outs[10] = {out->fW, out->fE, out->fS, out->fN, out->vol,
+                        out->psi, out->DW, out->DE, out->DS, out->DN};
+    for (int k = 0; k < 10; k++)
+      if (outs[k]) CK(cudaMemcpy(outs[k], *slots[k], b5, cudaMemcpyDeviceToHost));
+    if (out->quiet) CK(cudaMemcpy(out->quiet, qd, n, cudaMemcpyDeviceToHost));
+    if (out->rhoE_c || out->rhoE_fy) {
+      double *rc_d = nullptr, *rf_d = nullptr;
+      CK(cudaMalloc(&rc_d, n * sizeof(double)));
+      CK(cudaMalloc(&rf_d, (size_t)h->G.nxl * (h->G.ny + 1) * sizeof(double)));
+      k_profiles<<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P, rc_d, rf_d);
+      CK(cudaStreamSynchronize(h->stream));
+      if (out->rhoE_c) CK(cudaMemcpy(out->rhoE_c, rc_d, n * sizeof(double), cudaMemcpyDeviceToHost));
+      if (out->rhoE_fy)
+        CK(cudaMemcpy(out->rhoE_fy, rf_d, (size_t)h->G.nxl * (h->G.ny + 1) * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+      cudaFree(rc_d);
+      cudaFree(rf_d);
+    }
+  }
+  cudaFree(base);
+  cudaFree(qd);
+  return rc;
+}
+
+int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_error* err) {
+  if (!h) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  if (err) err->code = WB_ERR_NONE;
+  int mode = isnan(t_end) ? 0 : 1;
+  double tiny = mode ? 1.0e-12 * std::max(1.0, fabs(t_end)) : 0.0;
+  if (mode && !(h->t < t_end - tiny)) return WB_OK;  // run_until's loop does not execute
+  if (mode == 0 && max_steps < 0) {
+    g_err = "wb_run needs t_end or max_steps";
+    return WB_E_ARG;
+  }
+  if (h->need_prepare) {
+    wb_error e{};
+    int rc = do_prepare(h, nullptr, &e);
+    if (rc) return rc;
+    if (e.code != WB_ERR_NONE) {
+      if (err) *err = e;
+      return WB_OK;
+    }
+    h->need_prepare = false;
+  }
+  k_set_run<<<1, 1, 0, h->stream>>>(h->st, mode, 0, 0.0, mode ? t_end : 0.0, tiny,
+                                     max_steps, 1);
+  CK(cudaGetLastError());
+  if (chunk <= 0) chunk = 16;
+  if (!h->graph || h->graph_chunk != chunk) {
+    if (h->graph) cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < chunk; k++) enqueue_step(h);
+    CK(cudaStreamEndCapture(h->stream, &g));
+    CK(cudaGraphInstantiate(&h->graph, g, 0));
+    cudaGraphDestroy(g);
+    h->graph_chunk = chunk;
+  }
+  for (;;) {
+    CK(cudaGraphLaunch(h->graph, h->stream));
+    int rc = read_status(h);
+    if (rc) return rc;
+    if (h->h_st->stop != 0) break;
+  }
+  fill_error(h, err);
+  if (h->h_st->stop > 0) h->need_prepare = true;
+  return WB_OK;
+}
+
+int wb_get_status(wb_handle* h, wb_status* s) {
+  if (!h || !s) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  int rc = read_status(h);
+  if (rc) return rc;
+  const Status& d = *h->h_st;
+  s->t = d.t;
+  s->dt = d.dt;
+  unsigned long long b = d.rmax_used_bits;
+  memcpy(&s->rmax, &b, 8);
+  s->step = d.step;
+  s->stop = d.stop;
+  s->cur = d.cur;
+  s->n_second_order = d.n2nd;
+  s->x_faces_solved = d.nxs;
+  s->y_faces_solved = d.nys;
+  return WB_OK;
+}
+
+int wb_set_time(wb_handle* h, double t, int64_t step) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_set_time<<<1, 1, 0, h->stream>>>(h->st, t, step);
+  CK(cudaStreamSynchronize(h->stream));
+  h->t = t;
+  h->step = step;
+  return WB_OK;
+}
+
+int wb_get_dt_log(wb_handle* h, double* out, int64_t n) {
+  if (!h || !out || n < 0 || n > DTLOG_CAP) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(out, h->dtlog, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return WB_OK;
+}
+
+// ---- multi-GPU building blocks ----
+int wb_reduce_ptr(wb_handle* h, void** p) {
+  if (!h || !p) return WB_E_ARG;
+  *p = (void*)&h->st->red[0];
+  return WB_OK;
+}
+int wb_prepare_ptrs(wb_handle* h, void** rmax_bits, void** key_prep) {
+  if (!h) return WB_E_ARG;
+  if (rmax_bits) *rmax_bits = (void*)&h->st->rmax_bits;
+  if (key_prep) *key_prep = (void*)&h->st->key_prep;
+  return WB_OK;
+}
+int wb_prepare_local(wb_handle* h) {
+  if (!h || !h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  k_begin_prepare<<<1, 1, 0, h->stream>>>(h->st);
+  launch_detect(h);
+  if (h->g1)
+    k_prepare<true><<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P);
+  else
+    k_prepare<false><<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_check_prepare(wb_handle* h, double* rmax, wb_error* err) {
+  if (!h) return WB_E_ARG;
+  int rc = read_status(h);
+  if (rc) return rc;
+  Status& s = *h->h_st;
+  double r;
+  unsigned long long b = s.rmax_bits;
+  memcpy(&r, &b, 8);
+  if (rmax) *rmax = r;
+  if (err) {
+    err->code = WB_ERR_NONE;
+    err->i = err->j = -1;
+    err->step = s.step;
+    err->rmax = r;
+    if (s.key_prep != KEY_NONE) {
+      err->code = WB_ERR_CELL_STATE;
+      err->i = (int32_t)(s.key_prep / h->G.ny);
+      err->j = (int32_t)(s.key_prep % h->G.ny);
+    } else if (!(isfinite(r) && r > 0.0)) {
+      err->code = WB_ERR_WAVE_SPEED;
+    }
+  }
+  h->need_prepare = err && err->code != WB_ERR_NONE;
+  return WB_OK;
+}
+int wb_step_local(wb_handle* h, double max_dt, double t_end, int32_t mode) {
+  if (!h || !h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  int has = !isnan(max_dt);
+  double tiny = mode ? 1.0e-12 * std::max(1.0, fabs(t_end)) : 0.0;
+  k_set_run<<<1, 1, 0, h->stream>>>(h->st, mode, has, has ? max_dt : 0.0, t_end, tiny, -1, 0);
+  launch_detect(h);
+  k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
+  launch_step<false>(h, Dbg{});
+  k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_finalize(wb_handle* h) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_finalize<<<1, 1, 0, h->stream>>>(h->st, h->G.cfl, h->dtlog, DTLOG_CAP);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_halo_count(wb_handle* h, int64_t* n) {
+  if (!h || !n) return WB_E_ARG;
+  *n = 2LL * 4 * HALO * h->G.ny;
+  return WB_OK;
+}
+int wb_pack_halo(wb_handle* h, void* send) {
+  if (!h || !send) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_pack_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, (double*)send);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_unpack_halo(wb_handle* h, const void* recv, int32_t hl, int32_t hr) {
+  if (!h || !recv) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_unpack_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, (const double*)recv, hl, hr);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_sync(wb_handle* h) {
+  if (!h) return WB_E_ARG;
+  int rc = read_status(h);
+  return rc;
+}
+
+}  // extern "C"
