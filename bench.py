@@ -1,0 +1,261 @@
+"""Benchmark of the B200 time-stepping hot path (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric: FP64 cell updates per second (fluid cells x steps / device time), the
+reference's own throughput measure (timestepper.py:216-217) and the paper's
+"volumes processed per second".  Workload: the wall-impact dambreak (C5,
+SURVEY.md 8(d)) as an x-slab of 4096 x 16384 cells per GPU; with N GPUs the
+global grid is (4096 N) x 16384 over the same physical domain (weak scaling).
+The state (4.3 GB per GPU) is far larger than L2, so no flush is needed.
+
+--impl reference times the reference algorithm on the host CPU (the C
+restatement in oracle/, all host threads) on a bounded sample of the same
+workload; see DESIGN.md "Measurement".
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 cell updates/sec at 1/2/4/8 B200; % of HBM/FP64 roofline; CPU baseline"
+UNIT = "cell-updates/s"
+PUBLISHED = 2.0e7  # PAPER.md:26-27 "twenty million volumes/s"
+SLAB = (4096, 16384)
+HBM_BYTES_PER_CELL = 64.0  # read 4 + write 4 FP64 dynamic components
+
+
+def flops_per_step(n_fluid, n2nd, ex, ey):
+    """Algorithmic FP64 work of one step (dynamic counts of
+    the reference code paths)."""
+    return 224.0 * n_fluid + 125.0 * n2nd + 276.0 * ex + 494.0 * ey
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
+                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout
+                    self.samples.append([x.strip() for x in out.strip().split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 6
+                          for k in range(4) if "Active" in s[2 + k]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(seconds=12.0, res=(1024, 2048)):
+    """Reference algorithm (C oracle, all host threads) on a bounded sample of
+    the same workload: wall-impact over the same domain at a reduced grid."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc  # CPU-baseline leg only
+    from paper_1806_04960_b200.scenarios import build_scenario
+    cores = os.cpu_count() or 1
+    orc.set_threads(cores)
+    sc = build_scenario("wall-impact", res)
+    sim = orc.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
+    sim.advance()  # warm-up (page-in, thread pool)
+    n_fluid = sc.grid.fluid_cell_count()
+    t0 = time.perf_counter()
+    steps = 0
+    while time.perf_counter() - t0 < seconds and steps < 200:
+        sim.advance()
+        steps += 1
+    wall = time.perf_counter() - t0
+    return {"value": n_fluid * steps / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"wall-impact {res[0]}x{res[1]} (same domain), {steps} steps, "
+                      f"{wall:.1f} s, C restatement of the reference (oracle/), "
+                      f"{cores} OpenMP threads"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    samples = []
+    for _ in range(args.warmup):
+        cpu_baseline(seconds=2.0)
+    for _ in range(max(1, min(args.steps, 3))):
+        samples.append(cpu_baseline(seconds=8.0))
+    v = float(np.median([s["value"] for s in samples]))
+    base = samples[-1]
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": v / PUBLISHED,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "wall-impact (C5) dambreak, bounded CPU sample",
+                       "grid": [1024, 2048]},
+            "cpu_baseline": {**base, "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    from paper_1806_04960_b200 import _lib
+    from paper_1806_04960_b200.scenarios import build_scenario
+    from paper_1806_04960_b200.timestepper import Simulation
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_1806_04960_b200.distributed import run_bench_distributed
+        return run_bench_distributed(args)
+    dev = 0
+    torch.cuda.set_device(dev)
+    nx, ny = SLAB
+    sc = build_scenario("wall-impact", (nx, ny))
+    n_fluid = sc.grid.fluid_cell_count()
+    sim = Simulation(sc.grid, sc.params, sc.q0, sc.boundary, device=dev)
+    L = sim._L
+    stream = torch.cuda.Stream(device=dev)
+    _lib.check(L.wb_set_stream(sim._h, ctypes_void(stream.cuda_stream)), "wb_set_stream")
+    sim.run_steps(args.warmup, chunk=args.warmup)
+    # ---- timed region: K steps, device-side loop in CUDA-graph chunks ----
+    clocks = ClockSampler(dev)
+    clocks.start()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sim.run_steps(args.steps, chunk=max(d for d in range(1, 17) if args.steps % d == 0))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    ms_step = ms / args.steps
+    value = n_fluid * args.steps / (ms * 1e-3)
+    launches = 5 * args.steps
+    # ---- kernel-level roofline: k_step timed alone with CUDA events ----
+    import ctypes
+    md, mst, mtot = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    _lib.check(L.wb_profile_steps(sim._h, 5, ctypes.byref(md), ctypes.byref(mst),
+                                  ctypes.byref(mtot)), "wb_profile_steps")
+    wc = sim.work_counters()
+    F = flops_per_step(n_fluid, wc["n_second_order"], wc["x_faces"], wc["y_faces"])
+    tf = ctypes.c_double()
+    _lib.check(L.wb_fp64_peak(dev, ctypes.byref(tf)), "wb_fp64_peak")
+    fp64_achieved = F / (mst.value * 1e-3) / 1e12
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_achieved = HBM_BYTES_PER_CELL * n_fluid / (mst.value * 1e-3) / 1e9
+    t_hbm = HBM_BYTES_PER_CELL * n_fluid / (hbm_peak * 1e9)
+    t_fp64 = F / (tf.value * 1e12)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "kstep_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        if tj.get("grid") == [nx, ny]:
+            traffic = tj.get("dram_bytes_per_launch")
+    roof = {"bound": "fp64" if t_fp64 >= t_hbm else "hbm",
+            "achieved": fp64_achieved if t_fp64 >= t_hbm else hbm_achieved,
+            "peak": tf.value if t_fp64 >= t_hbm else hbm_peak,
+            "unit": "TFLOP/s" if t_fp64 >= t_hbm else "GB/s",
+            "traffic": traffic,
+            "kernel": "k_step (fused reconstruct + x/y faces + update)",
+            "kernel_ms": mst.value, "detect_ms": md.value, "pipeline_ms": mtot.value,
+            "share_of_step": mst.value / mtot.value if mtot.value else None,
+            "flop_per_step": F, "counters": wc,
+            "fp64_peak_source": "measured DFMA microbenchmark (wb_fp64_peak), burst",
+            "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm_achieved / hbm_peak,
+                    "bytes_per_cell": HBM_BYTES_PER_CELL},
+            "fp64": {"achieved": fp64_achieved, "peak": tf.value, "unit": "TFLOP/s",
+                     "frac": fp64_achieved / tf.value}}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    # ---- end to end through the public API with host buffers ----
+    q_host = torch.empty((nx, ny, 5), dtype=torch.float64, pin_memory=True).numpy()
+    q_host[...] = sc.q0
+    out_host = torch.empty((nx, ny, 5), dtype=torch.float64, pin_memory=True).numpy()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sim.q = q_host                      # H2D of the state
+    for _ in range(args.steps):
+        sim.advance()                   # per step: dt + status read back
+    sim._get_q(0, out=out_host)         # D2H of the result
+    e2e_wall = time.perf_counter() - t0
+    state_bytes = nx * ny * 5 * 8
+    e2e = {"value": n_fluid * args.steps / e2e_wall, "unit": UNIT,
+           "h2d_bytes_per_step": state_bytes / args.steps,
+           "d2h_bytes_per_step": state_bytes / args.steps + 32 + 96,
+           "api": "Simulation(q0 host) -> advance() x K -> sim.q (host)"}
+    base = cpu_baseline() if not args.no_cpu else None
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PUBLISHED,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "wall-impact (C5) dambreak, x-slab 4096x16384 per GPU",
+                       "grid": [nx, ny], "fluid_cells": n_fluid, "domain": [0, 3.2, 0, 1.8],
+                       "l2": "state 4.3 GB per GPU >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"x-slab dp{args.gpus}"},
+            "roofline": roof, "cpu_baseline": base, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
+def ctypes_void(p):
+    import ctypes
+    return ctypes.c_void_p(p)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -134,6 +134,15 @@ int wb_pack_halo(wb_handle* h, void* send_dev);
 int wb_unpack_halo(wb_handle* h, const void* recv_dev, int32_t have_left, int32_t have_right);
 int wb_sync(wb_handle* h);
 
+/* ---- measurement ---- */
+/* n steps launched one by one with CUDA events on the handle's stream:
+ * average device time of the detection kernel, the fused step kernel and the
+ * whole step pipeline (ms) */
+int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step,
+                     double* ms_total);
+/* measured FP64 FMA throughput of the device (TFLOP/s, 2 flop per DFMA) */
+int wb_fp64_peak(int32_t device, double* tflops);
+
 const char* wb_last_error(void);
 int wb_version(void);
 

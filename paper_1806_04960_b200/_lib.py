@@ -84,6 +84,8 @@ SIGNATURES = {
     "wb_pack_halo": [_H, _V],
     "wb_unpack_halo": [_H, _V, ctypes.c_int32, ctypes.c_int32],
     "wb_sync": [_H],
+    "wb_profile_steps": [_H, ctypes.c_int32, c_double_p, c_double_p, c_double_p],
+    "wb_fp64_peak": [ctypes.c_int32, c_double_p],
     "wb_version": [],
 }
 

@@ -141,7 +141,9 @@ static void launch_step(wb_handle* h, const Dbg& D) {
 }
 
 static void launch_detect(wb_handle* h) {
-  k_detect<<<(h->G.ncol + 127) / 128, 128, 0, h->stream>>>(h->G, h->B, h->P.dy);
+  // the pitch is a multiple of 32 and the mask is zero outside the domain,
+  // so whole 32-column groups can be streamed
+  k_detect_coop<<<h->G.pitch / 32, 256, 0, h->stream>>>(h->G, h->B, h->P.dy);
 }
 
 static void enqueue_step(wb_handle* h) {
@@ -711,6 +713,88 @@ int wb_unpack_halo(wb_handle* h, const void* recv, int32_t hl, int32_t hr) {
   CK(cudaGetLastError());
   return WB_OK;
 }
+// Kernel-level timing with CUDA events on the handle's stream: n steps
+// launched individually, average duration of the detect and step kernels.
+int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step,
+                     double* ms_total) {
+  if (!h || n <= 0 || !h->have_state) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  if (h->need_prepare) {
+    wb_error e{};
+    int rc = do_prepare(h, nullptr, &e);
+    if (rc) return rc;
+    if (e.code) return WB_E_STATE;
+    h->need_prepare = false;
+  }
+  cudaEvent_t ev[4];
+  for (int k = 0; k < 4; k++) CK(cudaEventCreate(&ev[k]));
+  k_set_run<<<1, 1, 0, h->stream>>>(h->st, 0, 0, 0.0, 0.0, 0.0, -1, 1);
+  double sd = 0, ss = 0;
+  float a, b;
+  CK(cudaEventRecord(ev[3], h->stream));
+  cudaEvent_t t0;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventRecord(t0, h->stream));
+  for (int k = 0; k < n; k++) {
+    CK(cudaEventRecord(ev[0], h->stream));
+    launch_detect(h);
+    CK(cudaEventRecord(ev[1], h->stream));
+    k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
+    CK(cudaEventRecord(ev[2], h->stream));
+    launch_step<false>(h, Dbg{});
+    CK(cudaEventRecord(ev[3], h->stream));
+    k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
+    k_finalize<<<1, 1, 0, h->stream>>>(h->st, h->G.cfl, h->dtlog, DTLOG_CAP);
+    CK(cudaEventSynchronize(ev[3]));
+    CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    CK(cudaEventElapsedTime(&b, ev[2], ev[3]));
+    sd += a;
+    ss += b;
+  }
+  cudaEvent_t t1;
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventRecord(t1, h->stream));
+  CK(cudaEventSynchronize(t1));
+  float tot;
+  CK(cudaEventElapsedTime(&tot, t0, t1));
+  for (int k = 0; k < 4; k++) cudaEventDestroy(ev[k]);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (ms_detect) *ms_detect = sd / n;
+  if (ms_step) *ms_step = ss / n;
+  if (ms_total) *ms_total = tot / n;
+  return read_status(h);
+}
+
+int wb_fp64_peak(int32_t device, double* tflops) {
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* out;
+  CK(cudaMalloc(&out, 8));
+  const int iters = 4096, threads = 256, blocks = sms * 8;
+  k_dfma_peak<<<blocks, threads>>>(out, 64, 1.0000001, 1e-7);  // warm-up
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int r = 0; r < 5; r++) {
+    CK(cudaEventRecord(e0));
+    k_dfma_peak<<<blocks, threads>>>(out, iters, 1.0000001, 1e-7);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  double flops = 2.0 * 64.0 * iters * (double)threads * blocks;
+  if (tflops) *tflops = flops / (best * 1e-3) / 1e12;
+  return WB_OK;
+}
+
 int wb_sync(wb_handle* h) {
   if (!h) return WB_E_ARG;
   int rc = read_status(h);
