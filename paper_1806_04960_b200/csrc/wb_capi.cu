@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <algorithm>
 #include <string>
@@ -98,6 +99,7 @@ struct wb_handle {
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
   dim3 grid_step;
+  int variant = 0;  // k_step launch configuration (WB_KSTEP_VARIANT, experiments)
 };
 
 static int ensure_tmp(wb_handle* h, size_t bytes) {
@@ -134,10 +136,23 @@ static void fill_error(wb_handle* h, wb_error* err) {
 
 template <bool DEBUG>
 static void launch_step(wb_handle* h, const Dbg& D) {
-  if (h->g1)
-    k_step<NT, true, DEBUG><<<h->grid_step, NT, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
-  else
-    k_step<NT, false, DEBUG><<<h->grid_step, NT, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+  if (!h->g1) {
+    k_step<64, 1, false, DEBUG><<<h->grid_step, 64, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+    return;
+  }
+  if (DEBUG) {
+    k_step<64, 1, true, true><<<h->grid_step, 64, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+    return;
+  }
+  const Geo& G = h->G;
+  switch (h->variant) {
+    case 1: k_step<64, 6, true, false><<<h->grid_step, 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 2: k_step<64, 8, true, false><<<h->grid_step, 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 3: k_step<128, 3, true, false><<<h->grid_step, 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 4: k_step<128, 4, true, false><<<h->grid_step, 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 5: k_step<32, 12, true, false><<<h->grid_step, 32, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    default: k_step<64, 1, true, false><<<h->grid_step, 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
+  }
 }
 
 static void launch_detect(wb_handle* h) {
@@ -257,7 +272,19 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   double c2r = cfg->gamma == 1.0 ? cfg->k0 / cfg->rho0
                                  : cfg->gamma * cfg->k0 / cfg->rho0 * pow(1.0, cfg->gamma - 1.0);
   P.vmax = 2.0 * sqrt(c2r);
+  P.c2c = P.cref * P.cref;
+  P.halfc = 0.5 / P.cref;
   h->g1 = cfg->gamma == 1.0;
+  {
+    double* d;
+    double hv[5];
+    CK(cudaMalloc(&d, 5 * sizeof(double)));
+    k_init_rcp<<<1, 1, 0, h->stream>>>(d, P.rho0, P.cref, P.c2c, P.dx, P.dy);
+    CK(cudaMemcpyAsync(hv, d, sizeof(hv), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(d);
+    P.yrho0 = hv[0]; P.ycref = hv[1]; P.yc2c = hv[2]; P.ydx = hv[3]; P.ydy = hv[4];
+  }
 
   const size_t plane = (size_t)G.pitch * G.ny;
   CK(cudaMalloc(&h->planes, 8 * plane * sizeof(double)));
@@ -315,8 +342,11 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   B.dtlog_cap = DTLOG_CAP;
 
   int L = cfg->rows_per_block > 0 ? cfg->rows_per_block : 64;
+  if (const char* v = getenv("WB_KSTEP_VARIANT")) h->variant = atoi(v);
+  const int nt = (h->variant == 3 || h->variant == 4) ? 128 : (h->variant == 5 ? 32 : 64);
+  if (!h->g1) h->variant = 0;
   // keep at least ~4 CTAs per SM on small grids
-  int bx = (G.nxl + NT - 2 * HALO - 1) / (NT - 2 * HALO);
+  int bx = (G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO);
   while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
   h->L = L;
   h->grid_step = dim3(bx, (G.ny + L - 1) / L);
@@ -792,6 +822,20 @@ int wb_fp64_peak(int32_t device, double* tflops) {
   cudaFree(out);
   double flops = 2.0 * 64.0 * iters * (double)threads * blocks;
   if (tflops) *tflops = flops / (best * 1e-3) / 1e12;
+  return WB_OK;
+}
+
+int wb_selftest_div(int32_t device, int64_t n, uint64_t seed, uint64_t* mismatches) {
+  CK(cudaSetDevice(device));
+  unsigned long long* d;
+  CK(cudaMalloc(&d, 8));
+  CK(cudaMemset(d, 0, 8));
+  k_selftest_div<<<148 * 8, 256>>>(n, seed, d);
+  CK(cudaGetLastError());
+  unsigned long long hv = 0;
+  CK(cudaMemcpy(&hv, d, 8, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  if (mismatches) *mismatches = hv;
   return WB_OK;
 }
 
