@@ -99,7 +99,7 @@ struct wb_handle {
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
   dim3 grid_step;
-  int variant = 0;  // k_step launch configuration (WB_KSTEP_VARIANT, experiments)
+  int variant = 3;  // k_step launch configuration (WB_KSTEP_VARIANT, experiments)
 };
 
 static int ensure_tmp(wb_handle* h, size_t bytes) {
