@@ -98,7 +98,6 @@ struct wb_handle {
   long long step = 0;
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
-  dim3 grid_step;
   int variant = 3;  // k_step launch configuration (WB_KSTEP_VARIANT, experiments)
 };
 
@@ -134,31 +133,35 @@ static void fill_error(wb_handle* h, wb_error* err) {
   }
 }
 
+static dim3 step_grid(const wb_handle* h, int nt) {
+  return dim3((h->G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO), (h->G.ny + h->L - 1) / h->L);
+}
+
 template <bool DEBUG>
 static void launch_step(wb_handle* h, const Dbg& D) {
+  const Geo& G = h->G;
   if (!h->g1) {
-    k_step<64, 1, false, DEBUG><<<h->grid_step, 64, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+    k_step<64, 1, false, DEBUG><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
     return;
   }
   if (DEBUG) {
-    k_step<64, 1, true, true><<<h->grid_step, 64, 0, h->stream>>>(h->G, h->B, h->P, h->L, D);
+    k_step<64, 1, true, true><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
     return;
   }
-  const Geo& G = h->G;
   switch (h->variant) {
-    case 1: k_step<64, 6, true, false><<<h->grid_step, 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 2: k_step<64, 8, true, false><<<h->grid_step, 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 3: k_step<128, 3, true, false><<<h->grid_step, 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 4: k_step<128, 4, true, false><<<h->grid_step, 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 5: k_step<32, 12, true, false><<<h->grid_step, 32, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    default: k_step<64, 1, true, false><<<h->grid_step, 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
+    case 1: k_step<64, 6, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 2: k_step<64, 8, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 3: k_step<128, 3, true, false><<<step_grid(h, 128), 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 4: k_step<128, 4, true, false><<<step_grid(h, 128), 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 5: k_step<32, 12, true, false><<<step_grid(h, 32), 32, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    default: k_step<64, 1, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
   }
 }
 
 static void launch_detect(wb_handle* h) {
   // the pitch is a multiple of 32 and the mask is zero outside the domain,
   // so whole 32-column groups can be streamed
-  k_detect_coop<<<h->G.pitch / 32, 256, 0, h->stream>>>(h->G, h->B, h->P.dy);
+  k_detect_coop<<<h->G.pitch / 32, 256, DET_SMEM, h->stream>>>(h->G, h->B, h->P.dy);
 }
 
 static void enqueue_step(wb_handle* h) {
@@ -222,6 +225,7 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
     CK(cudaMemcpyToSymbol(c_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
     tab_done[h->dev] = true;
   }
+  CK(cudaFuncSetAttribute(k_detect_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, DET_SMEM));
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
 
@@ -344,12 +348,10 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   int L = cfg->rows_per_block > 0 ? cfg->rows_per_block : 64;
   if (const char* v = getenv("WB_KSTEP_VARIANT")) h->variant = atoi(v);
   const int nt = (h->variant == 3 || h->variant == 4) ? 128 : (h->variant == 5 ? 32 : 64);
-  if (!h->g1) h->variant = 0;
   // keep at least ~4 CTAs per SM on small grids
   int bx = (G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO);
   while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
   h->L = L;
-  h->grid_step = dim3(bx, (G.ny + L - 1) / L);
   CK(cudaStreamSynchronize(h->stream));
   *out = h;
   return WB_OK;
