@@ -102,6 +102,8 @@ int wb_advance(wb_handle* h, double max_dt, double* dt_out, wb_error* err);
  * chunk = steps enqueued between host checks (captured in a CUDA graph). */
 int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_error* err);
 int wb_get_status(wb_handle* h, wb_status* s);
+/* the error that stopped the device-side run (code 0 if none) */
+int wb_get_error(wb_handle* h, wb_error* err);
 int wb_set_time(wb_handle* h, double t, int64_t step);
 /* per-step dt log written by the device (first `cap` steps) */
 int wb_get_dt_log(wb_handle* h, double* out, int64_t n);
@@ -118,13 +120,16 @@ int wb_advance_debug(wb_handle* h, double max_dt, double* dt_out, wb_error* err,
                      const wb_stage_arrays* out);
 
 /* ---- x-slab multi-GPU building blocks (driven by the host over NCCL) ---- */
-/* device address of the 2 x uint64 reduction vector [~errkey, rmax_bits]
- * (MAX-allreduce across ranks between wb_step_local and wb_finalize) */
+/* device address of the 2 x int64 reduction vector [enc(errkey), rate bits],
+ * enc(k) = 2^62 - k (0 = no error): a signed-int64 MAX allreduce across
+ * ranks between wb_step_local and wb_finalize yields the globally first
+ * failing cell (stage precedence included) and the global CFL rate */
 int wb_reduce_ptr(wb_handle* h, void** dev_ptr);
-/* device address of the current-state rate slot (uint64 bits, MAX) and of
- * the prepare-error key slot (uint64, MIN) used once after an upload */
 int wb_prepare_ptrs(wb_handle* h, void** rmax_bits, void** key_prep);
 int wb_prepare_local(wb_handle* h);         /* enqueue detect + prepare (no sync) */
+int wb_prepare_pack(wb_handle* h);          /* [enc(key_prep), rmax] -> reduction vector */
+int wb_prepare_unpack(wb_handle* h);        /* reduced vector -> key_prep, rmax */
+int wb_get_stream(wb_handle* h, void** cuda_stream);
 int wb_check_prepare(wb_handle* h, double* rmax, wb_error* err); /* sync + read */
 int wb_step_local(wb_handle* h, double max_dt, double t_end, int32_t mode);
 int wb_finalize(wb_handle* h);

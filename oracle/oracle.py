@@ -251,3 +251,220 @@ def time_steps(sim, n):
     t0 = time.perf_counter()
     sim.run_steps(n)
     return time.perf_counter() - t0
+
+
+# ---- x-slab backend for the distributed driver's CPU tests ----------------
+
+_ENC_TOP = 1 << 62
+
+
+def _enc(key):
+    return 0 if key is None else _ENC_TOP - key
+
+
+def _dec(e):
+    return None if e == 0 else _ENC_TOP - e
+
+
+def _bits(x):
+    return int(np.array([x], dtype=np.float64).view(np.int64)[0])
+
+
+def _unbits(b):
+    return float(np.array([b], dtype=np.int64).view(np.float64)[0])
+
+
+class OracleSlab:
+    """Slab backend of paper_1806_04960_b200.distributed.DistributedSimulation
+    on the CPU oracle (TEST INFRASTRUCTURE): holds the owned columns plus the
+    in-domain 2-column halo, runs the oracle kernels on that sub-grid and
+    mirrors the device status machine (k_prefinalize / k_finalize /
+    k_pack_halo / k_unpack_halo) exactly, so that the host logic of the
+    multi-GPU path can be checked over gloo on a CPU."""
+
+    HALO = 2
+
+    def __init__(self, grid, params, q_cols, col0, boundary, cfl, i0, i1):
+        import torch
+        from paper_1806_04960_b200.grid import BoundaryCondition, BoundarySpec, build_grid
+        nx, ny = grid.nx, grid.ny
+        self.nx, self.ny, self.i0, self.i1 = nx, ny, i0, i1
+        self.lo, self.hi = max(0, i0 - self.HALO), min(nx, i1 + self.HALO)
+        assert col0 <= self.lo and col0 + q_cols.shape[0] >= self.hi
+        self.q = np.ascontiguousarray(q_cols[self.lo - col0:self.hi - col0], dtype=np.float64)
+        refl = BoundaryCondition()
+        sub_b = BoundarySpec(left=boundary.left if self.lo == 0 else refl,
+                             right=boundary.right if self.hi == nx else refl,
+                             bottom=boundary.bottom, top=boundary.top)
+        x0 = float(grid.x0 + self.lo * grid.dx)
+        sub = type(grid)(self.hi - self.lo, ny, x0, grid.y0_origin, grid.dx, grid.dy,
+                         np.ascontiguousarray(np.asarray(grid.mask)[self.lo:self.hi]))
+        self.sim = OracleSimulation(sub, params, self.q, sub_b, cfl)
+        self.sim.xcent = np.ascontiguousarray(grid.x_centers[self.lo:self.hi])
+        self.cfl = float(cfl)
+        self.gdx, self.gdy, self.area = grid.dx, grid.dy, grid.cell_area
+        n = 2 * 4 * self.HALO * ny
+        self.red = torch.zeros(2, dtype=torch.int64)
+        self.send = torch.zeros(n, dtype=torch.float64)
+        self.recv = torch.zeros(n, dtype=torch.float64)
+        self.t, self.step, self.stop = 0.0, 0, 0
+        self.rmax = 0.0
+        self.err = (0, None, 0, 0.0)
+        self.key_prep = None
+        self.dt = 0.0
+
+    # owned columns in local indexing
+    def _owned(self):
+        return slice(self.i0 - self.lo, self.i1 - self.lo)
+
+    def _first_key(self, flags):
+        f = np.zeros_like(flags)
+        f[self._owned()] = flags[self._owned()]
+        bad = np.argwhere(f != 0)
+        if len(bad) == 0:
+            return None
+        i, j = (int(v) for v in bad[0])
+        return (i + self.lo) * self.ny + j
+
+    def prepare_local(self):
+        s = self.sim
+        s.q = self.q
+        s.flags[:] = 0
+        lib().wbo_prepare_step(ctypes.byref(s._cfg), _p(s.q), _p(s.mask), _p(s.yfaces),
+                               _p(s.ycent), _p(s.y0s), _p(s.aeqs), _p(s.y0s_prev),
+                               _p(s.rhoE_c), _p(s.rhoE_fy), _p(s.col_rate), _p(s.flags))
+        self.key_prep = self._first_key(s.flags)
+        self.rmax = float(s.col_rate[self._owned()].max())
+        self.stop = 0
+
+    def prepare_pack(self):
+        self.red[0] = _enc(self.key_prep)
+        self.red[1] = _bits(self.rmax)
+
+    def prepare_unpack(self):
+        self.key_prep = _dec(int(self.red[0]))
+        self.rmax = _unbits(int(self.red[1]))
+
+    def check_prepare(self):
+        code = 0
+        if self.key_prep is not None:
+            code = 1
+        elif not (np.isfinite(self.rmax) and self.rmax > 0.0):
+            code = 2
+        return self.rmax, code, self.key_prep
+
+    def step_local(self, max_dt, t_end, mode):
+        key_r = key_u = None
+        rnext = 0.0
+        if not self.stop and np.isfinite(self.rmax) and self.rmax > 0.0:
+            dt = self.cfl / self.rmax
+            if mode == 1:
+                mdt = t_end - self.t
+                if dt > mdt:
+                    dt = mdt
+            elif max_dt is not None and dt > max_dt:
+                dt = max_dt
+            self.dt = dt
+            s = self.sim
+            s.q = self.q
+            cfg = ctypes.byref(s._cfg)
+            L = lib()
+            # detection / profiles of the current state (prepare without flags)
+            fl = np.zeros_like(s.flags)
+            L.wbo_prepare_step(cfg, _p(s.q), _p(s.mask), _p(s.yfaces), _p(s.ycent), _p(s.y0s),
+                               _p(s.aeqs), _p(s.y0s_prev), _p(s.rhoE_c), _p(s.rhoE_fy),
+                               _p(s.col_rate), _p(fl))
+            s.flags[:] = 0
+            L.wbo_pass_reconstruct(cfg, _p(s.q), _p(s.mask), _p(s.aeqs), _p(s.rhoE_c),
+                                   _p(s.rhoE_fy), _p(s.ycent), _p(s.yfaces),
+                                   ctypes.c_double(0.5 * dt), _p(s.fW), _p(s.fE), _p(s.fS),
+                                   _p(s.fN), _p(s.vol), _p(s.psi), _p(s.quiet), _p(s.flags))
+            key_r = self._first_key(s.flags)
+            L.wbo_sweep_vertical(cfg, _p(s.mask), _p(s.ycent), _p(s.fW), _p(s.fE), _p(s.DW),
+                                 _p(s.DE), _p(s.y0s), _p(s.aeqs), _p(s.quiet))
+            L.wbo_sweep_horizontal(cfg, _p(s.mask), _p(s.xcent), _p(s.fS), _p(s.fN), _p(s.DS),
+                                   _p(s.DN), _p(s.y0s), _p(s.aeqs), _p(s.quiet))
+            s.flags[:] = 0
+            self.qn = np.zeros_like(self.q)
+            L.wbo_apply_update(cfg, _p(s.q), _p(self.qn), _p(s.mask), _p(s.fW), _p(s.fE),
+                               _p(s.fS), _p(s.fN), _p(s.DW), _p(s.DE), _p(s.DS), _p(s.DN),
+                               _p(s.vol), ctypes.c_double(dt / self.gdx),
+                               ctypes.c_double(dt / self.gdy), ctypes.c_double(dt / self.area),
+                               _p(s.flags))
+            key_u = self._first_key(s.flags)
+            # rate of the new state over owned fluid cells
+            fl[:] = 0
+            cr = np.zeros_like(s.col_rate)
+            L.wbo_prepare_step(cfg, _p(self.qn), _p(s.mask), _p(s.yfaces), _p(s.ycent),
+                               _p(np.zeros_like(s.y0s)), _p(np.ones_like(s.aeqs)),
+                               _p(np.full_like(s.y0s_prev, np.nan)),
+                               _p(np.zeros_like(s.rhoE_c)), _p(np.zeros_like(s.rhoE_fy)),
+                               _p(cr), _p(fl))
+            rnext = float(cr[self._owned()].max())
+        key = None
+        if key_r is not None:
+            key = (3 << 56) | key_r
+        elif key_u is not None:
+            key = (4 << 56) | key_u
+        self.red[0] = _enc(key)
+        self.red[1] = _bits(rnext)
+
+    def finalize(self):
+        if self.stop:
+            return
+        if not (np.isfinite(self.rmax) and self.rmax > 0.0):
+            self.stop = 2
+            self.err = (2, None, self.step, self.rmax)
+            return
+        key = _dec(int(self.red[0]))
+        if key is not None:
+            code = key >> 56
+            self.stop = code
+            self.err = (code, key & ((1 << 56) - 1), self.step, self.rmax)
+        else:
+            self.q = self.qn
+            self.t += self.dt
+            self.step += 1
+            self.rmax = _unbits(int(self.red[1]))
+
+    def _halo_cols(self, side):
+        H = self.HALO
+        if side == 0:
+            return [self.i0 + h - self.lo for h in range(H)]
+        return [self.i1 - H + h - self.lo for h in range(H)]
+
+    def pack_halo(self):
+        if self.stop > 0:
+            return
+        H, ny = self.HALO, self.ny
+        buf = np.zeros((2, 4, H, ny))
+        for side in range(2):
+            for h, c in enumerate(self._halo_cols(side)):
+                if 0 <= c < self.q.shape[0]:
+                    buf[side, :, h, :] = self.q[c, :, :4].T
+        self.send.copy_(__import__("torch").from_numpy(buf.ravel()))
+
+    def unpack_halo(self, have_left, have_right):
+        if self.stop > 0:
+            return
+        H, ny = self.HALO, self.ny
+        buf = self.recv.numpy().reshape(2, 4, H, ny)
+        if have_left:
+            for h in range(H):
+                self.q[self.i0 - H + h - self.lo, :, :4] = buf[0, :, h, :].T
+        if have_right:
+            for h in range(H):
+                self.q[self.i1 + h - self.lo, :, :4] = buf[1, :, h, :].T
+
+    def status(self):
+        return {"t": self.t, "dt": self.dt, "step": self.step, "stop": self.stop,
+                "rmax": self.rmax}
+
+    def last_error(self):
+        return self.err
+
+    def cell_q(self, i, j):
+        return self.q[i - self.lo, j].copy()
+
+    def owned_state(self):
+        return self.q[self._owned()].copy()

@@ -70,6 +70,7 @@ SIGNATURES = {
     "wb_advance": [_H, ctypes.c_double, c_double_p, ctypes.POINTER(WbError)],
     "wb_run": [_H, ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(WbError)],
     "wb_get_status": [_H, ctypes.POINTER(WbStatus)],
+    "wb_get_error": [_H, ctypes.POINTER(WbError)],
     "wb_set_time": [_H, ctypes.c_double, ctypes.c_int64],
     "wb_get_dt_log": [_H, c_double_p, ctypes.c_int64],
     "wb_advance_debug": [_H, ctypes.c_double, c_double_p, ctypes.POINTER(WbError),
@@ -77,6 +78,9 @@ SIGNATURES = {
     "wb_reduce_ptr": [_H, ctypes.POINTER(_V)],
     "wb_prepare_ptrs": [_H, ctypes.POINTER(_V), ctypes.POINTER(_V)],
     "wb_prepare_local": [_H],
+    "wb_prepare_pack": [_H],
+    "wb_prepare_unpack": [_H],
+    "wb_get_stream": [_H, ctypes.POINTER(_V)],
     "wb_check_prepare": [_H, c_double_p, ctypes.POINTER(WbError)],
     "wb_step_local": [_H, ctypes.c_double, ctypes.c_double, ctypes.c_int32],
     "wb_finalize": [_H],

@@ -620,6 +620,15 @@ int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_erro
   return WB_OK;
 }
 
+int wb_get_error(wb_handle* h, wb_error* err) {
+  if (!h || !err) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  int rc = read_status(h);
+  if (rc) return rc;
+  fill_error(h, err);
+  return WB_OK;
+}
+
 int wb_get_status(wb_handle* h, wb_status* s) {
   if (!h || !s) return WB_E_ARG;
   CK(cudaSetDevice(h->dev));
@@ -667,6 +676,25 @@ int wb_prepare_ptrs(wb_handle* h, void** rmax_bits, void** key_prep) {
   if (!h) return WB_E_ARG;
   if (rmax_bits) *rmax_bits = (void*)&h->st->rmax_bits;
   if (key_prep) *key_prep = (void*)&h->st->key_prep;
+  return WB_OK;
+}
+int wb_prepare_pack(wb_handle* h) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_prepare_pack<<<1, 1, 0, h->stream>>>(h->st);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_prepare_unpack(wb_handle* h) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_prepare_unpack<<<1, 1, 0, h->stream>>>(h->st);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_get_stream(wb_handle* h, void** s) {
+  if (!h || !s) return WB_E_ARG;
+  *s = (void*)h->stream;
   return WB_OK;
 }
 int wb_prepare_local(wb_handle* h) {

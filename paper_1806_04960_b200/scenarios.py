@@ -31,6 +31,7 @@ class Scenario:
     boundary: BoundarySpec
     q0: np.ndarray          # (nx, ny, 5) conserved state, reference layout
     t_end: float = None
+    col0: int = 0           # first global column held in q0 (x-slab builds)
 
 
 def detect_columns(alpha, mask, y_faces, dy):
@@ -47,13 +48,15 @@ def detect_columns(alpha, mask, y_faces, dy):
     return ylow + ssum * dy, aeq
 
 
-def column_equilibrium_state(grid, params, alpha, u=None, v=None, gas_rho=None):
+def column_equilibrium_state(grid, params, alpha, u=None, v=None, gas_rho=None, cols=None):
     """Conserved state for a volume-fraction field: liquid density follows
     each column's detected equilibrium aeq*eq_rho(y, y0); gas (alpha <= 10 eps
-    when ``gas_rho`` is given) gets rho = gas_rho."""
-    nx, ny = grid.nx, grid.ny
+    when ``gas_rho`` is given) gets rho = gas_rho.  ``alpha`` covers the
+    columns ``cols = (lo, hi)`` (all columns by default)."""
+    lo, hi = cols if cols is not None else (0, grid.nx)
+    nx, ny = hi - lo, grid.ny
     yc = grid.y_centers
-    y0s, aeqs = detect_columns(alpha, grid.mask, grid.y_faces, grid.dy)
+    y0s, aeqs = detect_columns(alpha, np.asarray(grid.mask)[lo:hi], grid.y_faces, grid.dy)
     rho_a = np.empty((nx, ny))
     # one libm-exp profile per distinct surface level (few in practice)
     for y0 in np.unique(y0s):
@@ -74,20 +77,21 @@ def column_equilibrium_state(grid, params, alpha, u=None, v=None, gas_rho=None):
     return q
 
 
-def _centres(grid):
-    return np.meshgrid(grid.x_centers, grid.y_centers, indexing="ij")
+def _centres(grid, cols=None):
+    lo, hi = cols if cols is not None else (0, grid.nx)
+    return np.meshgrid(grid.x_centers[lo:hi], grid.y_centers, indexing="ij")
 
 
 def _box(x, y, x0, x1, y0, y1):
     return (x >= x0) & (x <= x1) & (y >= y0) & (y <= y1)
 
 
-def _dambreak(grid, params, region, gas_rho=None):
+def _dambreak(grid, params, region, gas_rho=None, cols=None):
     eps = params.epsilon
-    x, y = _centres(grid)
+    x, y = _centres(grid, cols)
     liquid = _box(x, y, *region)
     alpha = np.where(liquid, 1.0 - eps, eps)
-    return column_equilibrium_state(grid, params, alpha,
+    return column_equilibrium_state(grid, params, alpha, cols=cols,
                                     gas_rho=params.rho0 if gas_rho is None else gas_rho)
 
 
@@ -115,7 +119,7 @@ LAKE_OBSTACLES = ((-0.25, 0.25, 0.0, 0.33), (0.30, 0.40, 0.0, 0.60),
                   (-0.45, -0.35, 0.0, 0.17))
 
 
-def build_scenario(name, resolution=None, seed=0):
+def build_scenario(name, resolution=None, seed=0, columns=None):
     """Build one named configuration.
 
     * ``dambreak-dry``  -- C1, [-50,50]x[0,4], liquid [-50,0]x[0,1.4618], k0 6.37e5
@@ -132,14 +136,25 @@ def build_scenario(name, resolution=None, seed=0):
     * ``jet``           -- small inflow case (inflow segment on the left side,
       transmissive right/top) that exercises the inflow ghost.
     * ``tait7``         -- a gamma = 7 dambreak (pow() path; parity by tolerance).
+
+    ``columns=(lo, hi)`` builds only those columns of q0 (x-slab of a
+    multi-GPU run; supported by the dambreak-type scenarios); the grid is
+    always the global one.
     """
+    if columns is not None and name not in ("dambreak-dry", "weir", "wall-impact"):
+        sc = build_scenario(name, resolution, seed)
+        lo, hi = columns
+        sc.q0 = np.ascontiguousarray(sc.q0[lo:hi])
+        sc.col0 = lo
+        return sc
+    cols = columns
     if name == "dambreak-dry":
         res = resolution or (200, 100)
         params = ModelParams(k0=6.37e5)
         grid = build_grid((-50.0, 50.0, 0.0, 4.0), res)
-        q = _dambreak(grid, params, (-50.0, 0.0, 0.0, 1.4618))
+        q = _dambreak(grid, params, (-50.0, 0.0, 0.0, 1.4618), cols=cols)
         bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
-        return Scenario(name, grid, params, bnd, q)
+        return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
     if name == "lake":
         return _lake(name, resolution or (2048, 1024), LAKE_OBSTACLES)
     if name == "equilibrium-obstacle":
@@ -167,15 +182,15 @@ def build_scenario(name, resolution=None, seed=0):
         params = ModelParams(k0=6.54e5)
         dx = 15.0 / res[0]
         grid = build_grid((-7.5, 7.5, 0.0, 2.1), res, [(0.0, dx, 0.0, 0.7)])
-        q = _dambreak(grid, params, (-7.5, 0.0, 0.0, 1.5))
-        return Scenario(name, grid, params, BoundarySpec(), q)
+        q = _dambreak(grid, params, (-7.5, 0.0, 0.0, 1.5), cols=cols)
+        return Scenario(name, grid, params, BoundarySpec(), q, col0=cols[0] if cols else 0)
     if name == "wall-impact":
         res = resolution or (32768, 16384)
         params = ModelParams(k0=2.62e5)
         grid = build_grid((0.0, 3.2, 0.0, 1.8), res)
-        q = _dambreak(grid, params, (0.0, 1.2, 0.0, 0.6))
+        q = _dambreak(grid, params, (0.0, 1.2, 0.0, 0.6), cols=cols)
         bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
-        return Scenario(name, grid, params, bnd, q)
+        return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
     if name == "jet":
         res = resolution or (96, 64)
         params = ModelParams(k0=2.78e5, g=9.81)

@@ -1,0 +1,102 @@
+"""x-slab device path on one GPU (GPU test).
+
+Several DeviceSlab handles (i_begin/i_end subsets of one grid, each on its own
+stream) are stepped in one process; the collectives of the multi-GPU driver
+are emulated on the host (MAX of the reduction vectors, halo buffers copied
+between neighbours), never by kernels that wait on each other.  The owned
+columns must match the single-domain oracle bit for bit, including the error
+stop of the 200x100 dambreak at step 309."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _slabs(torch, scen, res, world):
+    from paper_1806_04960_b200.distributed import DeviceSlab, slab_bounds, stored_range
+    from paper_1806_04960_b200.scenarios import build_scenario
+    out = []
+    for r in range(world):
+        i0, i1 = slab_bounds(res[0], world, r)
+        lo, hi = stored_range(res[0], i0, i1)
+        sc = build_scenario(scen, res, columns=(lo, hi))
+        out.append(DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0))
+    return out
+
+
+def _reduce(torch, slabs):
+    torch.cuda.synchronize()
+    red = torch.stack([s.red for s in slabs]).max(dim=0).values
+    for s in slabs:
+        s.red.copy_(red)
+    torch.cuda.synchronize()
+
+
+def _halo(torch, slabs):
+    for s in slabs:
+        with s.stream_ctx():
+            s.pack_halo()
+    torch.cuda.synchronize()
+    W = len(slabs)
+    half = slabs[0].send.numel() // 2
+    for r, s in enumerate(slabs):
+        if r > 0:
+            s.recv[:half].copy_(slabs[r - 1].send[half:])
+        if r < W - 1:
+            s.recv[half:].copy_(slabs[r + 1].send[:half])
+    torch.cuda.synchronize()
+    for r, s in enumerate(slabs):
+        s.unpack_halo(r > 0, r < W - 1)
+    torch.cuda.synchronize()
+
+
+def _run(torch, slabs, steps):
+    for s in slabs:
+        s.prepare_local()
+        s.prepare_pack()
+    _reduce(torch, slabs)
+    for s in slabs:
+        s.prepare_unpack()
+    for s in slabs:
+        assert s.check_prepare()[1] == 0
+    for _ in range(steps):
+        for s in slabs:
+            s.step_local(None, None, 0)
+        _reduce(torch, slabs)
+        for s in slabs:
+            s.finalize()
+        _halo(torch, slabs)
+        st = [s.status() for s in slabs]
+        if st[0]["stop"] > 0:
+            return [s.last_error() for s in slabs]
+    return None
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_slabs_bitexact(torch_cuda, oracle, world):
+    from paper_1806_04960_b200.scenarios import build_scenario
+    res = (131, 70)
+    slabs = _slabs(torch_cuda, "wall-impact", res, world)
+    assert _run(torch_cuda, slabs, 15) is None
+    q = np.concatenate([s.owned_state() for s in slabs], axis=0)
+    sc = build_scenario("wall-impact", res)
+    ref = oracle.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
+    ref.run_steps(15)
+    assert np.array_equal(q, ref.q)
+    assert all(s.status()["t"] == ref.t for s in slabs)
+
+
+def test_device_slabs_error_stop(torch_cuda):
+    slabs = _slabs(torch_cuda, "dambreak-dry", (200, 100), 2)
+    errs = _run(torch_cuda, slabs, 400)
+    assert errs is not None
+    for code, key, step, _ in errs:
+        assert (code, divmod(key, 100), step) == (4, (98, 37), 309)
