@@ -49,43 +49,42 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the
+    timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu=0):
         self.gpu = gpu
-        self.samples = []
-        self._stop = threading.Event()
-        self._th = None
+        self.proc = None
 
     def start(self):
-        def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
-                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout
-                    self.samples.append([x.strip() for x in out.strip().split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
-        self._th = threading.Thread(target=run, daemon=True)
-        self._th.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)  # let the sampler start before the timed region
+        except OSError:
+            self.proc = None
 
     def stop(self):
-        self._stop.set()
-        if self._th:
-            self._th.join(timeout=10)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
-        reasons = sorted({names[k] for s in self.samples if len(s) >= 6
-                          for k in range(4) if "Active" in s[2 + k]})
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        time.sleep(0.1)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [[x.strip() for x in ln.split(",")] for ln in out.splitlines() if ln.strip()]
+        rows = [r for r in rows if len(r) >= 6]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[k] for r in rows for k in range(4) if r[2 + k] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(rows)}
 
 
 def cpu_baseline(seconds=12.0, res=(1024, 2048)):

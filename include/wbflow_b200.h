@@ -148,6 +148,8 @@ int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step
 /* self-test of the inlined IEEE division against a/b on n pseudo-random
  * operand pairs (bit patterns, zeros, all binades, subnormals) */
 int wb_selftest_div(int32_t device, int64_t n, uint64_t seed, uint64_t* mismatches);
+/* the device exp() used by eq_rho (glibc 2.39 restatement) on n host values */
+int wb_eval_exp(int32_t device, const double* x, double* y, int64_t n);
 /* measured FP64 FMA throughput of the device (TFLOP/s, 2 flop per DFMA) */
 int wb_fp64_peak(int32_t device, double* tflops);
 

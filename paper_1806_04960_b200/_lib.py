@@ -90,6 +90,7 @@ SIGNATURES = {
     "wb_sync": [_H],
     "wb_profile_steps": [_H, ctypes.c_int32, c_double_p, c_double_p, c_double_p],
     "wb_fp64_peak": [ctypes.c_int32, c_double_p],
+    "wb_eval_exp": [ctypes.c_int32, c_double_p, c_double_p, ctypes.c_int64],
     "wb_selftest_div": [ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
                         ctypes.POINTER(ctypes.c_uint64)],
     "wb_version": [],

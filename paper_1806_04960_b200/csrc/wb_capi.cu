@@ -412,7 +412,8 @@ int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
     src = h->tmp;
   }
   CK(cudaMemsetAsync(h->scratch, 0xff, sizeof(unsigned long long), h->stream));
-  k_aos_to_planes<<<148 * 8, 256, 0, h->stream>>>(h->G, h->B, src, i_first, n_cols, h->scratch);
+  k_aos_to_planes<<<dim3((n_cols + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
+      h->G, h->B, src, i_first, n_cols, h->scratch);
   CK(cudaGetLastError());
   unsigned long long bad = 0;
   CK(cudaMemcpyAsync(&bad, h->scratch, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -445,7 +446,8 @@ int wb_get_state_buf(wb_handle* h, double* q, int32_t which, int32_t is_device) 
     if (rc) return rc;
     dst = h->tmp;
   }
-  k_planes_to_aos<<<148 * 8, 256, 0, h->stream>>>(h->G, h->B, dst, which ? 1 : -1);
+  k_planes_to_aos<<<dim3((h->G.nxl + TT - 1) / TT, (h->G.ny + TT - 1) / TT), 256, 0,
+                    h->stream>>>(h->G, h->B, dst, which ? 1 : -1);
   CK(cudaGetLastError());
   if (!is_device) CK(cudaMemcpyAsync(q, dst, bytes, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -866,6 +868,26 @@ int wb_selftest_div(int32_t device, int64_t n, uint64_t seed, uint64_t* mismatch
   CK(cudaMemcpy(&hv, d, 8, cudaMemcpyDeviceToHost));
   cudaFree(d);
   if (mismatches) *mismatches = hv;
+  return WB_OK;
+}
+
+int wb_eval_exp(int32_t device, const double* x, double* y, int64_t n) {
+  if (!x || !y || n <= 0) return WB_E_ARG;
+  CK(cudaSetDevice(device));
+  static bool tab_ok = false;
+  if (!tab_ok) {
+    CK(cudaMemcpyToSymbol(c_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
+    tab_ok = true;
+  }
+  double *dx, *dy;
+  CK(cudaMalloc(&dx, n * sizeof(double)));
+  CK(cudaMalloc(&dy, n * sizeof(double)));
+  CK(cudaMemcpy(dx, x, n * sizeof(double), cudaMemcpyHostToDevice));
+  k_eval_exp<<<148 * 4, 256>>>(dx, dy, n);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(dx);
+  cudaFree(dy);
   return WB_OK;
 }
 
