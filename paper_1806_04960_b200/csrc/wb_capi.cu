@@ -289,6 +289,16 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
     cudaFree(d);
     P.yrho0 = hv[0]; P.ycref = hv[1]; P.yc2c = hv[2]; P.ydx = hv[3]; P.ydy = hv[4];
   }
+  {
+    // FastDiv::divc assumes positive constant divisors in [2^-100, 2^100]
+    const double lo = ldexp(1.0, -100), hi = ldexp(1.0, 100);
+    const double cs[5] = {P.rho0, P.cref, P.c2c, P.dx, P.dy};
+    for (double v : cs)
+      if (!(v >= lo && v <= hi)) {
+        g_err = "rho0, c, c^2, dx, dy must lie in [2^-100, 2^100]";
+        return WB_E_ARG;
+      }
+  }
 
   const size_t plane = (size_t)G.pitch * G.ny;
   CK(cudaMalloc(&h->planes, 8 * plane * sizeof(double)));
