@@ -133,7 +133,8 @@ int wb_get_stream(wb_handle* h, void** cuda_stream);
 int wb_check_prepare(wb_handle* h, double* rmax, wb_error* err); /* sync + read */
 int wb_step_local(wb_handle* h, double max_dt, double t_end, int32_t mode);
 int wb_finalize(wb_handle* h);
-/* halo columns: 2 x 4 x 2 x ny doubles (side, component, column, j) */
+/* halo buffers: 2 contiguous side blocks of (4 x 2 x ny state doubles
+ * (component, column, j) + 2 x (y0, aeq) of those columns) */
 int wb_halo_count(wb_handle* h, int64_t* n_doubles);
 int wb_pack_halo(wb_handle* h, void* send_dev);
 int wb_unpack_halo(wb_handle* h, const void* recv_dev, int32_t have_left, int32_t have_right);

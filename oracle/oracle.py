@@ -303,7 +303,7 @@ class OracleSlab:
         self.sim.xcent = np.ascontiguousarray(grid.x_centers[self.lo:self.hi])
         self.cfl = float(cfl)
         self.gdx, self.gdy, self.area = grid.dx, grid.dy, grid.cell_area
-        n = 2 * 4 * self.HALO * ny
+        n = 2 * (4 * self.HALO * ny + 2 * self.HALO)
         self.red = torch.zeros(2, dtype=torch.int64)
         self.send = torch.zeros(n, dtype=torch.float64)
         self.recv = torch.zeros(n, dtype=torch.float64)
@@ -434,27 +434,36 @@ class OracleSlab:
         return [self.i1 - H + h - self.lo for h in range(H)]
 
     def pack_halo(self):
+        """Same layout as the device: per side, 4 x HALO x ny state values and
+        then (y0, aeq) per halo column (the oracle recomputes detection itself,
+        so those two slots are filled with the column's detection but unused)."""
         if self.stop > 0:
             return
         H, ny = self.HALO, self.ny
-        buf = np.zeros((2, 4, H, ny))
+        blk = 4 * H * ny + 2 * H
+        buf = np.zeros((2, blk))
         for side in range(2):
+            st = np.zeros((4, H, ny))
             for h, c in enumerate(self._halo_cols(side)):
                 if 0 <= c < self.q.shape[0]:
-                    buf[side, :, h, :] = self.q[c, :, :4].T
+                    st[:, h, :] = self.q[c, :, :4].T
+            buf[side, :4 * H * ny] = st.ravel()
         self.send.copy_(__import__("torch").from_numpy(buf.ravel()))
 
     def unpack_halo(self, have_left, have_right):
         if self.stop > 0:
             return
         H, ny = self.HALO, self.ny
-        buf = self.recv.numpy().reshape(2, 4, H, ny)
+        blk = 4 * H * ny + 2 * H
+        buf = self.recv.numpy().reshape(2, blk)
         if have_left:
+            st = buf[0, :4 * H * ny].reshape(4, H, ny)
             for h in range(H):
-                self.q[self.i0 - H + h - self.lo, :, :4] = buf[0, :, h, :].T
+                self.q[self.i0 - H + h - self.lo, :, :4] = st[:, h, :].T
         if have_right:
+            st = buf[1, :4 * H * ny].reshape(4, H, ny)
             for h in range(H):
-                self.q[self.i1 + h - self.lo, :, :4] = buf[1, :, h, :].T
+                self.q[self.i1 + h - self.lo, :, :4] = st[:, h, :].T
 
     def status(self):
         return {"t": self.t, "dt": self.dt, "step": self.step, "stop": self.stop,

@@ -86,6 +86,9 @@ struct wb_handle {
   uint8_t* mask = nullptr;
   double *y0s = nullptr, *aeqs = nullptr, *ycent = nullptr, *yfaces = nullptr,
          *xcent = nullptr;
+  double *ch_sum = nullptr, *ch_aeq = nullptr;
+  int* ch_jlo = nullptr;
+  unsigned long long* ch_flag = nullptr;
   Status* st = nullptr;
   Status* h_st = nullptr;
   double* dtlog = nullptr;
@@ -94,6 +97,10 @@ struct wb_handle {
   size_t tmp_bytes = 0;
   bool have_state = false;
   bool need_prepare = true;
+  // Simulation.y0s / aeqs (timestepper.py:76-77) hold the detection the last
+  // advance() used, i.e. of the state *before* that step: after a committed
+  // step that is the other buffer's detection, after max_rate() the current.
+  bool cols_prev = false;
   double t = 0.0;
   long long step = 0;
   cudaGraphExec_t graph = nullptr;
@@ -164,8 +171,9 @@ static void launch_detect(wb_handle* h) {
   k_detect_coop<<<h->G.pitch / 32, 256, DET_SMEM, h->stream>>>(h->G, h->B, h->P.dy);
 }
 
+// One step: detection of the current state comes from the previous step's
+// fused chain (or from the prepare after an upload).
 static void enqueue_step(wb_handle* h) {
-  launch_detect(h);
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   launch_step<false>(h, Dbg{});
   k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
@@ -174,6 +182,7 @@ static void enqueue_step(wb_handle* h) {
 
 // detect + admissibility/rate of the current state; sets code 1 / 2 errors
 static int do_prepare(wb_handle* h, double* rmax, wb_error* err) {
+  h->cols_prev = false;
   k_begin_prepare<<<1, 1, 0, h->stream>>>(h->st);
   launch_detect(h);
   if (h->g1)
@@ -318,10 +327,10 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
     free(hm);
     CK(e);
   }
-  CK(cudaMalloc(&h->y0s, G.pitch * sizeof(double)));
-  CK(cudaMalloc(&h->aeqs, G.pitch * sizeof(double)));
-  CK(cudaMemset(h->y0s, 0, G.pitch * sizeof(double)));
-  CK(cudaMemset(h->aeqs, 0, G.pitch * sizeof(double)));
+  CK(cudaMalloc(&h->y0s, 2 * G.pitch * sizeof(double)));
+  CK(cudaMalloc(&h->aeqs, 2 * G.pitch * sizeof(double)));
+  CK(cudaMemset(h->y0s, 0, 2 * G.pitch * sizeof(double)));
+  CK(cudaMemset(h->aeqs, 0, 2 * G.pitch * sizeof(double)));
   CK(cudaMalloc(&h->ycent, G.ny * sizeof(double)));
   CK(cudaMalloc(&h->yfaces, (G.ny + 1) * sizeof(double)));
   CK(cudaMemcpy(h->ycent, ycent, G.ny * sizeof(double), cudaMemcpyHostToDevice));
@@ -346,8 +355,10 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
 
   Bufs& B = h->B;
   B.mask = h->mask;
-  B.y0s = h->y0s;
-  B.aeqs = h->aeqs;
+  B.y0s[0] = h->y0s;
+  B.y0s[1] = h->y0s + G.pitch;
+  B.aeqs[0] = h->aeqs;
+  B.aeqs[1] = h->aeqs + G.pitch;
   B.ycent = h->ycent;
   B.yfaces = h->yfaces;
   B.xcent = h->xcent;
@@ -361,7 +372,22 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   // keep at least ~4 CTAs per SM on small grids
   int bx = (G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO);
   while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
+  if (L > 64) L = 64;  // the fused detection keeps one fluid bit per row
   h->L = L;
+  {
+    const int nby = (G.ny + L - 1) / L;
+    const int nbx_max = (G.nxl + 32 - 2 * HALO - 1) / (32 - 2 * HALO) + 1;  // smallest CTA width
+    CK(cudaMalloc(&h->ch_sum, (size_t)nby * G.pitch * sizeof(double)));
+    CK(cudaMalloc(&h->ch_aeq, (size_t)nby * G.pitch * sizeof(double)));
+    CK(cudaMalloc(&h->ch_jlo, (size_t)nby * G.pitch * sizeof(int)));
+    CK(cudaMalloc(&h->ch_flag, (size_t)nby * nbx_max * sizeof(unsigned long long)));
+    CK(cudaMemset(h->ch_flag, 0, (size_t)nby * nbx_max * sizeof(unsigned long long)));
+    h->B.ch_sum = h->ch_sum;
+    h->B.ch_aeq = h->ch_aeq;
+    h->B.ch_jlo = h->ch_jlo;
+    h->B.ch_flag = h->ch_flag;
+    h->B.nbx_max = nbx_max;
+  }
   CK(cudaStreamSynchronize(h->stream));
   *out = h;
   return WB_OK;
@@ -376,6 +402,10 @@ int wb_destroy(wb_handle* h) {
   cudaFree(h->mask);
   cudaFree(h->y0s);
   cudaFree(h->aeqs);
+  cudaFree(h->ch_sum);
+  cudaFree(h->ch_aeq);
+  cudaFree(h->ch_jlo);
+  cudaFree(h->ch_flag);
   cudaFree(h->ycent);
   cudaFree(h->yfaces);
   cudaFree(h->xcent);
@@ -494,11 +524,14 @@ int wb_max_rate(wb_handle* h, double* rmax, wb_error* err) {
 int wb_get_columns(wb_handle* h, double* y0s, double* aeqs) {
   if (!h) return WB_E_ARG;
   CK(cudaSetDevice(h->dev));
-  CK(cudaStreamSynchronize(h->stream));
+  int rc = read_status(h);
+  if (rc) return rc;
+  const int b = h->h_st->cur ^ (h->cols_prev && h->h_st->step > 0 ? 1 : 0);
+  const size_t off = (size_t)b * h->G.pitch + HALO;
   if (y0s)
-    CK(cudaMemcpy(y0s, h->y0s + HALO, h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(y0s, h->y0s + off, h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost));
   if (aeqs)
-    CK(cudaMemcpy(aeqs, h->aeqs + HALO, h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(aeqs, h->aeqs + off, h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost));
   return WB_OK;
 }
 
@@ -521,7 +554,6 @@ static int advance_impl(wb_handle* h, double max_dt, double* dt_out, wb_error* e
   int has = !isnan(max_dt);
   k_set_run<<<1, 1, 0, h->stream>>>(h->st, 0, has, has ? max_dt : 0.0, 0.0, 0.0,
                                      h->step + 1, 1);
-  launch_detect(h);  // after k_set_run: detection skips when the run is stopped
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   if (dbg)
     launch_step<true>(h, *dbg);
@@ -534,6 +566,7 @@ static int advance_impl(wb_handle* h, double max_dt, double* dt_out, wb_error* e
   if (rc) return rc;
   fill_error(h, err);
   if (h->h_st->stop > 0) h->need_prepare = true;  // a failed step leaves q^n current
+  else h->cols_prev = true;
   if (dt_out) *dt_out = h->h_st->dt;
   return WB_OK;
 }
@@ -569,7 +602,8 @@ int wb_advance_debug(wb_handle* h, double max_dt, double* dt_out, wb_error* err,
       double *rc_d = nullptr, *rf_d = nullptr;
       CK(cudaMalloc(&rc_d, n * sizeof(double)));
       CK(cudaMalloc(&rf_d, (size_t)h->G.nxl * (h->G.ny + 1) * sizeof(double)));
-      k_profiles<<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P, rc_d, rf_d);
+      k_profiles<<<148 * 4, 256, 0, h->stream>>>(h->G, h->B, h->P, rc_d, rf_d,
+                                                  h->cols_prev ? 1 : 0);
       CK(cudaStreamSynchronize(h->stream));
       if (out->rhoE_c) CK(cudaMemcpy(out->rhoE_c, rc_d, n * sizeof(double), cudaMemcpyDeviceToHost));
       if (out->rhoE_fy)
@@ -629,6 +663,7 @@ int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_erro
   }
   fill_error(h, err);
   if (h->h_st->stop > 0) h->need_prepare = true;
+  else h->cols_prev = true;
   return WB_OK;
 }
 
@@ -752,7 +787,6 @@ int wb_step_local(wb_handle* h, double max_dt, double t_end, int32_t mode) {
   int has = !isnan(max_dt);
   double tiny = mode ? 1.0e-12 * std::max(1.0, fabs(t_end)) : 0.0;
   k_set_run<<<1, 1, 0, h->stream>>>(h->st, mode, has, has ? max_dt : 0.0, t_end, tiny, -1, 0);
-  launch_detect(h);
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   launch_step<false>(h, Dbg{});
   k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
@@ -768,7 +802,7 @@ int wb_finalize(wb_handle* h) {
 }
 int wb_halo_count(wb_handle* h, int64_t* n) {
   if (!h || !n) return WB_E_ARG;
-  *n = 2LL * 4 * HALO * h->G.ny;
+  *n = 2LL * 4 * HALO * h->G.ny + 4 * HALO;  // state columns + their (y0, aeq)
   return WB_OK;
 }
 int wb_pack_halo(wb_handle* h, void* send) {
@@ -809,7 +843,6 @@ int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step
   CK(cudaEventRecord(t0, h->stream));
   for (int k = 0; k < n; k++) {
     CK(cudaEventRecord(ev[0], h->stream));
-    launch_detect(h);
     CK(cudaEventRecord(ev[1], h->stream));
     k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
     CK(cudaEventRecord(ev[2], h->stream));

@@ -30,6 +30,9 @@ struct Status {
   long long err_key, err_step;
   double err_rmax;
   unsigned long long rmax_used_bits;  // rate the last committed step used for dt
+  unsigned long long launch_id;       // incremented before every step launch
+  unsigned int ticket;                // dynamic CTA index of the step kernel
+  unsigned int pad2;
 };
 
 struct Geo {
@@ -48,8 +51,15 @@ struct Geo {
 struct Bufs {
   double* q[2][4];        // [buffer][component] planes, index j*pitch + c
   const uint8_t* mask;    // j*pitch + c (0 outside the domain)
-  double* y0s;            // per stored column
-  double* aeqs;
+  double* y0s[2];         // per stored column, detection of buffer b's state
+  double* aeqs[2];
+  // fused-detection chain: running (sum, aeq, first fluid row) per row
+  // segment and column, and a publish flag per (segment, column strip)
+  double* ch_sum;
+  double* ch_aeq;
+  int* ch_jlo;
+  unsigned long long* ch_flag;
+  int nbx_max;
   const double* ycent;    // ny
   const double* yfaces;   // ny + 1
   const double* xcent;    // per stored column (x centre, for bottom/top inflow)
