@@ -102,6 +102,12 @@ int wb_advance(wb_handle* h, double max_dt, double* dt_out, wb_error* err);
  * chunk = steps enqueued between host checks (captured in a CUDA graph). */
 int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_error* err);
 int wb_get_status(wb_handle* h, wb_status* s);
+/* Device diagnostics of the current state (deterministic reduction):
+ * out9 = {total mass (sum alpha*rho * dx*dy, cf. Simulation.total_mass,
+ * timestepper.py:127-130), max|u|, max|v|, min alpha, max alpha,
+ * E_rho, E_u, E_v, E_P} where the E_* are max-norm errors against the exact
+ * water-at-rest profile of surface level y0_eq (NaN skips) */
+int wb_diagnostics(wb_handle* h, double y0_eq, double* out9);
 /* the error that stopped the device-side run (code 0 if none) */
 int wb_get_error(wb_handle* h, wb_error* err);
 int wb_set_time(wb_handle* h, double t, int64_t step);

@@ -71,6 +71,7 @@ SIGNATURES = {
     "wb_run": [_H, ctypes.c_double, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(WbError)],
     "wb_get_status": [_H, ctypes.POINTER(WbStatus)],
     "wb_get_error": [_H, ctypes.POINTER(WbError)],
+    "wb_diagnostics": [_H, ctypes.c_double, c_double_p],
     "wb_set_time": [_H, ctypes.c_double, ctypes.c_int64],
     "wb_get_dt_log": [_H, c_double_p, ctypes.c_int64],
     "wb_advance_debug": [_H, ctypes.c_double, c_double_p, ctypes.POINTER(WbError),

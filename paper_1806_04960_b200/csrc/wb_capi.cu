@@ -667,6 +667,23 @@ int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_erro
   return WB_OK;
 }
 
+int wb_diagnostics(wb_handle* h, double y0_eq, double* out9) {
+  if (!h || !out9) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  const int nblk = 148 * 2;
+  double* d;
+  CK(cudaMalloc(&d, (size_t)(nblk + 1) * DIAG_N * sizeof(double)));
+  k_diag1<<<nblk, DIAG_T, 0, h->stream>>>(h->G, h->B, h->P, y0_eq, d);
+  k_diag2<<<1, 1, 0, h->stream>>>(d, nblk, h->P.area, d + (size_t)nblk * DIAG_N);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out9, d + (size_t)nblk * DIAG_N, DIAG_N * sizeof(double),
+                     cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFree(d);
+  return WB_OK;
+}
+
 int wb_get_error(wb_handle* h, wb_error* err) {
   if (!h || !err) return WB_E_ARG;
   CK(cudaSetDevice(h->dev));

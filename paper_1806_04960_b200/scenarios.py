@@ -86,6 +86,33 @@ def _box(x, y, x0, x1, y0, y1):
     return (x >= x0) & (x <= x1) & (y >= y0) & (y <= y1)
 
 
+def _liquid_state(grid, params, liquid, u=None, v=None):
+    """Conserved state for a g = 0 case: rho = rho0 everywhere, alpha =
+    1-eps in the liquid (velocity (u, v) there) and eps in the gas (at rest)."""
+    eps = params.epsilon
+    alpha = np.where(liquid, 1.0 - eps, eps)
+    q = np.zeros(alpha.shape + (5,))
+    q[..., 0] = alpha * params.rho0
+    if u is not None:
+        q[..., 1] = np.where(liquid, q[..., 0] * u, 0.0)
+    if v is not None:
+        q[..., 2] = np.where(liquid, q[..., 0] * v, 0.0)
+    q[..., 3] = alpha
+    q[..., 4] = grid.y_centers[None, :]
+    return q
+
+
+def _dambreak_multi(grid, params, regions, cols=None):
+    """Dambreak with several liquid rectangles (wet bed / step cases)."""
+    eps = params.epsilon
+    x, y = _centres(grid, cols)
+    liquid = np.zeros(x.shape, dtype=bool)
+    for r in regions:
+        liquid |= _box(x, y, *r)
+    alpha = np.where(liquid, 1.0 - eps, eps)
+    return column_equilibrium_state(grid, params, alpha, cols=cols, gas_rho=params.rho0)
+
+
 def _dambreak(grid, params, region, gas_rho=None, cols=None):
     eps = params.epsilon
     x, y = _centres(grid, cols)
@@ -135,13 +162,19 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
       transmissive top.
     * ``jet``           -- small inflow case (inflow segment on the left side,
       transmissive right/top) that exercises the inflow ghost.
+    * ``dambreak-wet`` / ``dambreak-step-dry`` / ``dambreak-step-wet`` -- PAPER.md
+      section 5.6.2-5.6.4 (wet bed, 0.2 bottom step).
+    * ``equilibrium-flat`` -- the paper's flat-bottom lake at rest (100x100).
+    * ``spinning-square`` / ``jet-plate`` -- PAPER.md sections 5.3 / 5.4 (g = 0).
     * ``tait7``         -- a gamma = 7 dambreak (pow() path; parity by tolerance).
 
     ``columns=(lo, hi)`` builds only those columns of q0 (x-slab of a
     multi-GPU run; supported by the dambreak-type scenarios); the grid is
     always the global one.
     """
-    if columns is not None and name not in ("dambreak-dry", "weir", "wall-impact"):
+    if columns is not None and name not in ("dambreak-dry", "weir", "wall-impact",
+                                            "dambreak-wet", "dambreak-step-dry",
+                                            "dambreak-step-wet"):
         sc = build_scenario(name, resolution, seed)
         lo, hi = columns
         sc.q0 = np.ascontiguousarray(sc.q0[lo:hi])
@@ -155,6 +188,48 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
         q = _dambreak(grid, params, (-50.0, 0.0, 0.0, 1.4618), cols=cols)
         bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
         return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
+    if name in ("dambreak-wet", "dambreak-step-dry", "dambreak-step-wet"):
+        # PAPER.md section 5.6.2-5.6.4 (Omega = [-50,50]x[0,4], step [0,50]x[0,0.2])
+        res = resolution or (4000, 400)
+        wet = name != "dambreak-step-dry"
+        params = ModelParams(k0=6.54e5 if wet else 6.37e5)
+        step = name.startswith("dambreak-step")
+        grid = build_grid((-50.0, 50.0, 0.0, 4.0), res,
+                          [(0.0, 50.0, 0.0, 0.2)] if step else ())
+        if name == "dambreak-wet":
+            regions = [(-50.0, 0.0, 0.0, 1.5), (0.0, 50.0, 0.0, 0.75)]
+        elif name == "dambreak-step-dry":
+            regions = [(-50.0, 0.0, 0.0, 0.4618)]
+        else:
+            regions = [(-50.0, 0.0, 0.0, 0.4618), (0.0, 50.0, 0.2, 0.50873)]
+        q = _dambreak_multi(grid, params, regions, cols=cols)
+        bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
+        return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
+    if name == "equilibrium-flat":
+        return _lake(name, resolution or (100, 100), ())
+    if name == "spinning-square":
+        # PAPER.md section 5.3: [-5,5]^2, square [-1,1]^2, u = (2 pi y, -2 pi x), k0 8.78e5, g 0
+        res = resolution or (850, 850)
+        params = ModelParams(k0=8.78e5, g=0.0)
+        grid = build_grid((-5.0, 5.0, -5.0, 5.0), res)
+        x, y = _centres(grid)
+        liquid = _box(x, y, -1.0, 1.0, -1.0, 1.0)
+        q = _liquid_state(grid, params, liquid, 2.0 * math.pi * y, -2.0 * math.pi * x)
+        return Scenario(name, grid, params, BoundarySpec(), q)
+    if name == "jet-plate":
+        # PAPER.md section 5.4: [-6,8]x[0,10], strip -2 <= y - sqrt(3) x <= 0,
+        # |u| = 5 along the jet towards the plate y = 0, k0 2.78e5, g 0
+        res = resolution or (500, 350)
+        params = ModelParams(k0=2.78e5, g=0.0)
+        grid = build_grid((-6.0, 8.0, 0.0, 10.0), res)
+        x, y = _centres(grid)
+        s3 = math.sqrt(3.0)
+        liquid = (y - s3 * x <= 0.0) & (y - s3 * x >= -2.0)
+        q = _liquid_state(grid, params, liquid, -5.0 * 0.5, -5.0 * s3 / 2.0)
+        bnd = BoundarySpec(left=BoundaryCondition("transmissive"),
+                           right=BoundaryCondition("transmissive"),
+                           top=BoundaryCondition("transmissive"))
+        return Scenario(name, grid, params, bnd, q)
     if name == "lake":
         return _lake(name, resolution or (2048, 1024), LAKE_OBSTACLES)
     if name == "equilibrium-obstacle":
@@ -218,5 +293,6 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
     raise ValueError(f"unknown scenario {name!r}")
 
 
-SCENARIOS = ("dambreak-dry", "lake", "equilibrium-obstacle", "perturbed-lake", "drop",
-             "weir", "wall-impact", "jet", "tait7")
+SCENARIOS = ("dambreak-dry", "dambreak-wet", "dambreak-step-dry", "dambreak-step-wet", "lake",
+             "equilibrium-flat", "equilibrium-obstacle", "perturbed-lake", "drop",
+             "spinning-square", "jet-plate", "weir", "wall-impact", "jet", "tait7")

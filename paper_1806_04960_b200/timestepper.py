@@ -236,9 +236,31 @@ class Simulation:
             np.multiply((rho / pr.rho0) ** pr.gamma - 1.0, pr.k0, out=p, where=fluid)
         return rho, u, v, alpha, p
 
-    def total_mass(self):
-        """sum(alpha rho) * cell area over fluid cells (timestepper.py:127-130)."""
+    def total_mass(self, device=False):
+        """sum(alpha rho) * cell area over fluid cells (timestepper.py:127-130).
+
+        The default downloads q and sums with numpy exactly like the
+        reference; ``device=True`` uses the on-device deterministic reduction
+        (no download; equal to ~1e-15 relative, different summation order)."""
+        if device:
+            return self.diagnostics()["mass"]
         return float(np.sum(self.q[:, :, 0][self._fluid]) * self.grid.cell_area)
+
+    def diagnostics(self, y0_eq=None):
+        """Device-side reductions of the current state: mass, max |u|, max |v|,
+        alpha range and -- given the surface level ``y0_eq`` of the exact
+        water-at-rest profile -- the paper's equilibrium errors E_rho, E_u, E_v,
+        E_P (PAPER.md:866-886)."""
+        out = np.empty(9)
+        check(self._L.wb_diagnostics(self._h, math.nan if y0_eq is None else float(y0_eq),
+                                     dptr(out)), "wb_diagnostics")
+        keys = ("mass", "max_u", "max_v", "min_alpha", "max_alpha", "E_rho", "E_u", "E_v",
+                "E_P")
+        d = dict(zip(keys, (float(v) for v in out)))
+        if y0_eq is None:
+            for k in keys[5:]:
+                d.pop(k)
+        return d
 
     # ---- errors -------------------------------------------------------------
     def _raise(self, e):

@@ -100,6 +100,10 @@ CASES = [
     ("tait7_64x32", "tait7", (64, 32), True, (30,), (), {}),
     ("lake_64x32", "lake", (64, 32), False, (200,), (), {}),
     ("impact_200x100", "wall-impact", (200, 100), False, (), (1, 50, 150), {}),
+    ("stepwet_200x40", "dambreak-step-wet", (200, 40), True, (1, 40), (), {}),
+    ("spinsq_48", "spinning-square", (48, 48), True, (1, 30), (), {}),
+    ("jetplate_56x40", "jet-plate", (56, 40), False, (30,), (), {}),
+    ("eqflat_100", "equilibrium-flat", (100, 100), False, (100,), (), {}),
     ("dambreak_200x100", "dambreak-dry", (200, 100), False, (), (1, 10, 100, 250),
      {"run_to_error": 400}),
 ]
