@@ -174,6 +174,7 @@ static void launch_detect(wb_handle* h) {
 // One step: detection of the current state comes from the previous step's
 // fused chain (or from the prepare after an upload).
 static void enqueue_step(wb_handle* h) {
+  if (!h->B.fuse_detect) launch_detect(h);
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   launch_step<false>(h, Dbg{});
   k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
@@ -371,7 +372,9 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   const int nt = (h->variant == 3 || h->variant == 4) ? 128 : (h->variant == 5 ? 32 : 64);
   // keep at least ~4 CTAs per SM on small grids
   int bx = (G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO);
-  while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
+  if (const char* v = getenv("WB_ROWS")) L = atoi(v);
+  else if (cfg->rows_per_block <= 0)
+    while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
   if (L > 64) L = 64;  // the fused detection keeps one fluid bit per row
   h->L = L;
   {
@@ -387,6 +390,11 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
     h->B.ch_jlo = h->ch_jlo;
     h->B.ch_flag = h->ch_flag;
     h->B.nbx_max = nbx_max;
+    // Fused (chained) detection pays ~1-3 us per row segment on the critical
+    // path; the separate column-sequential detect pays ~1.7 us per 32 rows.
+    // Chain when the columns are long relative to the segment count.
+    h->B.fuse_detect = G.ny >= 2048 ? 1 : 0;
+    if (const char* v = getenv("WB_FUSE_DETECT")) h->B.fuse_detect = atoi(v) ? 1 : 0;
   }
   CK(cudaStreamSynchronize(h->stream));
   *out = h;
@@ -541,6 +549,7 @@ static int advance_impl(wb_handle* h, double max_dt, double* dt_out, wb_error* e
   if (!h->have_state) return WB_E_STATE;
   CK(cudaSetDevice(h->dev));
   if (err) err->code = WB_ERR_NONE;
+  bool prepared_now = false;
   if (h->need_prepare) {
     wb_error e{};
     int rc = do_prepare(h, nullptr, &e);
@@ -550,10 +559,12 @@ static int advance_impl(wb_handle* h, double max_dt, double* dt_out, wb_error* e
       return WB_OK;
     }
     h->need_prepare = false;
+    prepared_now = true;
   }
   int has = !isnan(max_dt);
   k_set_run<<<1, 1, 0, h->stream>>>(h->st, 0, has, has ? max_dt : 0.0, 0.0, 0.0,
                                      h->step + 1, 1);
+  if (!h->B.fuse_detect && !prepared_now) launch_detect(h);
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   if (dbg)
     launch_step<true>(h, *dbg);
@@ -804,6 +815,7 @@ int wb_step_local(wb_handle* h, double max_dt, double t_end, int32_t mode) {
   int has = !isnan(max_dt);
   double tiny = mode ? 1.0e-12 * std::max(1.0, fabs(t_end)) : 0.0;
   k_set_run<<<1, 1, 0, h->stream>>>(h->st, mode, has, has ? max_dt : 0.0, t_end, tiny, -1, 0);
+  if (!h->B.fuse_detect) launch_detect(h);
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   launch_step<false>(h, Dbg{});
   k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
@@ -860,6 +872,7 @@ int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step
   CK(cudaEventRecord(t0, h->stream));
   for (int k = 0; k < n; k++) {
     CK(cudaEventRecord(ev[0], h->stream));
+    if (!h->B.fuse_detect) launch_detect(h);
     CK(cudaEventRecord(ev[1], h->stream));
     k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
     CK(cudaEventRecord(ev[2], h->stream));

@@ -60,6 +60,7 @@ struct Bufs {
   int* ch_jlo;
   unsigned long long* ch_flag;
   int nbx_max;
+  int fuse_detect;  // 1: detection of q^{n+1} is chained inside k_step; 0: k_detect per step
   const double* ycent;    // ny
   const double* yfaces;   // ny + 1
   const double* xcent;    // per stored column (x centre, for bottom/top inflow)
