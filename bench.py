@@ -143,6 +143,10 @@ def run_ours(args):
     if world > 1:
         from paper_1806_04960_b200.distributed import run_bench_distributed
         return run_bench_distributed(args)
+    if args.gpus != 1:
+        sys.stderr.write("bench.py: --gpus > 1 needs torchrun (one process per GPU); "
+                         "running the single-GPU benchmark\n")
+        args.gpus = 1
     dev = 0
     torch.cuda.set_device(dev)
     nx, ny = SLAB
