@@ -14,7 +14,7 @@
 #include <string>
 #include "../../include/wbflow_b200.h"
 #include "wb_kernels.cuh"
-#include "wb_step.cu"  // single translation unit: kernels + c_exp_tab
+#include "wb_step.cu"  // single translation unit: kernels + g_exp_tab
 
 
 using namespace wb;
@@ -235,7 +235,7 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   CK(cudaSetDevice(h->dev));
   static bool tab_done[64] = {false};
   if (h->dev < 64 && !tab_done[h->dev]) {
-    CK(cudaMemcpyToSymbol(c_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
+    CK(cudaMemcpyToSymbol(g_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
     tab_done[h->dev] = true;
   }
   CK(cudaFuncSetAttribute(k_detect_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, DET_SMEM));
@@ -953,7 +953,7 @@ int wb_eval_exp(int32_t device, const double* x, double* y, int64_t n) {
   CK(cudaSetDevice(device));
   static bool tab_ok = false;
   if (!tab_ok) {
-    CK(cudaMemcpyToSymbol(c_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
+    CK(cudaMemcpyToSymbol(g_exp_tab, WB_EXP_TAB, sizeof(WB_EXP_TAB)));
     tab_ok = true;
   }
   double *dx, *dy;
