@@ -163,6 +163,8 @@ static void launch_step(wb_handle* h, const Dbg& D) {
     case 5: k_step<32, 12, true, false><<<step_grid(h, 32), 32, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
     case 6: k_step<128, 2, true, false><<<step_grid(h, 128), 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
     case 7: k_step<96, 4, true, false><<<step_grid(h, 96), 96, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 8: k_step_r<64, 200, true><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
+    case 9: k_step_r<64, 224, true><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
 
     default: k_step<64, 1, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
   }
@@ -372,8 +374,8 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
 
   int L = cfg->rows_per_block > 0 ? cfg->rows_per_block : 64;
   if (const char* v = getenv("WB_KSTEP_VARIANT")) h->variant = atoi(v);
-  static const int nts[9] = {64, 64, 64, 128, 128, 32, 128, 96, 192};
-  const int nt = (h->variant >= 0 && h->variant < 9) ? nts[h->variant] : 64;
+  static const int nts[10] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64};
+  const int nt = (h->variant >= 0 && h->variant < 10) ? nts[h->variant] : 64;
   // keep at least ~4 CTAs per SM on small grids
   int bx = (G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO);
   if (const char* v = getenv("WB_ROWS")) L = atoi(v);
