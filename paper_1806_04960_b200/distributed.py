@@ -190,20 +190,27 @@ class DistributedSimulation:
 
     # -- collectives ------------------------------------------------------
     def _allreduce_max(self, t):
+        if t.is_cuda and not self._nccl:  # gloo with device slabs: stage through host
+            h = t.cpu()
+            self.dist.all_reduce(h, op=self.dist.ReduceOp.MAX, group=self.group)
+            t.copy_(h)
+            return
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
 
     def _halo_exchange(self):
         be, r, W = self.be, self.rank, self.world
         be.pack_halo()
         half = be.send.numel() // 2
+        staged = be.send.is_cuda and not self._nccl  # gloo: point-to-point on host copies
+        send, recv = (be.send.cpu(), be.recv.cpu()) if staged else (be.send, be.recv)
         ops = []
         P2P = self.dist.P2POp
         if r > 0:
-            ops.append(P2P(self.dist.isend, be.send[:half], r - 1, self.group))
-            ops.append(P2P(self.dist.irecv, be.recv[:half], r - 1, self.group))
+            ops.append(P2P(self.dist.isend, send[:half], r - 1, self.group))
+            ops.append(P2P(self.dist.irecv, recv[:half], r - 1, self.group))
         if r < W - 1:
-            ops.append(P2P(self.dist.isend, be.send[half:], r + 1, self.group))
-            ops.append(P2P(self.dist.irecv, be.recv[half:], r + 1, self.group))
+            ops.append(P2P(self.dist.isend, send[half:], r + 1, self.group))
+            ops.append(P2P(self.dist.irecv, recv[half:], r + 1, self.group))
         if ops:
             if self._nccl:
                 for w in self.dist.batch_isend_irecv(ops):
@@ -212,6 +219,8 @@ class DistributedSimulation:
                 reqs = [op.op(op.tensor, op.peer, op.group) for op in ops]
                 for q in reqs:
                     q.wait()
+        if staged:
+            be.recv.copy_(recv)
         be.unpack_halo(r > 0, r < W - 1)
 
     def _ctx(self):
@@ -257,7 +266,7 @@ class DistributedSimulation:
         owner = self.be.i0 <= i < self.be.i1
         q = self.be.cell_q(i, j) if owner else np.zeros(5)
         dev = self.be.red.device
-        t = torch.tensor(q, dtype=torch.float64, device=dev)
+        t = torch.tensor(q, dtype=torch.float64, device=dev if self._nccl else "cpu")
         with self._ctx():
             self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()

@@ -48,3 +48,62 @@ def test_nccl_world1_matches_simulation():
         assert dsim.t == sim.t and np.array_equal(be.owned_state(), sim.q)
     finally:
         dist.destroy_process_group()
+
+
+def _gloo_worker(rank, world, port, scen, res, steps, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from paper_1806_04960_b200.distributed import (DeviceSlab, DistributedSimulation,
+                                                   slab_bounds, stored_range)
+    from paper_1806_04960_b200.errors import SimulationError
+    from paper_1806_04960_b200.scenarios import build_scenario
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    i0, i1 = slab_bounds(res[0], world, rank)
+    lo, hi = stored_range(res[0], i0, i1)
+    sc = build_scenario(scen, res, columns=(lo, hi))
+    be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
+    dsim = DistributedSimulation(be, sc.grid)
+    err = None
+    try:
+        dsim.run_steps(steps, check_every=7)
+    except SimulationError as e:
+        err = (str(e), e.step, e.cell)
+    np.savez(os.path.join(out, f"rank{rank}.npz"), q=be.owned_state(), t=dsim.t,
+             step=dsim.step_count, err=np.array(repr(err)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scen,res,steps", [("wall-impact", (300, 160), 25),
+                                            ("dambreak-dry", (200, 100), 400)])
+def test_device_slabs_two_processes_gloo(scen, res, steps):
+    """The full multi-process driver (torch.distributed, two ranks, device
+    slabs on cuda:0, collectives staged through host memory by gloo) against
+    the single-handle Simulation: same state, t and step; on the dry dambreak
+    the same abort (step 309, cell (98, 37)) on both ranks."""
+    import tempfile
+    import torch
+    import torch.multiprocessing as mp
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1806_04960_b200.errors import SimulationError
+    from paper_1806_04960_b200.scenarios import build_scenario
+    from paper_1806_04960_b200.timestepper import Simulation
+    out = tempfile.mkdtemp()
+    mp.spawn(_gloo_worker, args=(2, _port(), scen, res, steps, out), nprocs=2, join=True)
+    parts = [np.load(os.path.join(out, f"rank{r}.npz")) for r in range(2)]
+    full = build_scenario(scen, res)
+    sim = Simulation(full.grid, full.params, full.q0, full.boundary)
+    err = None
+    try:
+        sim.run_steps(steps)
+    except SimulationError as e:
+        err = (str(e), e.step, e.cell)
+    for p in parts:
+        assert str(p["err"]) == repr(err)
+        assert float(p["t"]) == sim.t and int(p["step"]) == sim.step_count
+    assert np.array_equal(np.concatenate([p["q"] for p in parts], axis=0), sim.q)
+    if scen == "dambreak-dry":
+        assert err is not None and err[1] == 309 and err[2] == (98, 37)
