@@ -58,7 +58,7 @@ class ClockSampler:
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu=0):
-        self.gpu = gpu
+        self.gpu = gpu  # index or comma-separated list of indices
         self.proc = None
 
     def start(self):
@@ -141,8 +141,7 @@ def run_ours(args):
     from paper_1806_04960_b200.timestepper import Simulation
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        from paper_1806_04960_b200.distributed import run_bench_distributed
-        return run_bench_distributed(args)
+        return run_ours_distributed(args)
     if args.gpus != 1:
         sys.stderr.write("bench.py: --gpus > 1 needs torchrun (one process per GPU); "
                          "running the single-GPU benchmark\n")
@@ -170,7 +169,8 @@ def run_ours(args):
     clk = clocks.stop()
     ms_step = ms / args.steps
     value = n_fluid * args.steps / (ms * 1e-3)
-    launches = 4 * args.steps  # reset_counters, k_step, prefinalize, finalize per step
+    # per step reset_counters, k_step, prefinalize, finalize; one set_run per wb_run call
+    launches = 4 * args.steps + 1
     # ---- kernel-level roofline: k_step timed alone with CUDA events ----
     import ctypes
     md, mst, mtot = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
@@ -239,6 +239,117 @@ def run_ours(args):
             "clocks": clk}
     print(json.dumps(line), flush=True)
 
+
+
+def run_ours_distributed(args):
+    """N > 1 ranks under torchrun, one GPU each: the wall-impact x-slab of
+    4096 x 16384 cells per rank, global grid (4096 N) x 16384 (weak scaling).
+    K steps of the multi-rank driver (NCCL halo send/recv + one MAX all-reduce
+    per step), device time = max over ranks of the CUDA-event time on each
+    rank's stream.  WB_DIST_BACKEND=gloo (host-staged collectives) exists only
+    to exercise this path with several ranks on one GPU; it is not a
+    benchmark configuration."""
+    import ctypes
+    import torch
+    import torch.distributed as dist
+    from paper_1806_04960_b200.distributed import (DeviceSlab, DistributedSimulation,
+                                                   slab_bounds, stored_range)
+    from paper_1806_04960_b200.scenarios import build_scenario
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("WB_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    else:
+        dist.init_process_group(backend)
+    nx, ny = SLAB[0] * world, SLAB[1]
+    i0, i1 = slab_bounds(nx, world, rank)
+    lo, hi = stored_range(nx, i0, i1)
+    sc = build_scenario("wall-impact", (nx, ny), columns=(lo, hi))
+    be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, dev)
+    sim = DistributedSimulation(be, sc.grid)
+    sim.run_steps(args.warmup)
+    clocks = ClockSampler(",".join(str(d) for d in range(min(world, torch.cuda.device_count())))
+                          ) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(be.stream)
+    for _ in range(args.steps):
+        sim._enqueue_step()
+    e1.record(be.stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if clocks else None
+
+    def allmax(x):
+        t = torch.tensor([float(x)], dtype=torch.float64,
+                         device=f"cuda:{dev}" if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = allmax(e0.elapsed_time(e1))
+    s = sim._sync()
+    sim._check(s)
+    n_fluid = int(np.count_nonzero(np.asarray(sc.grid.mask)))
+    value = n_fluid * args.steps / (ms * 1e-3)
+    # kernel roofline on this rank's slab (k_step timed alone, after the timed region)
+    n2, ex, ey = s["counters"]
+    md, mst, mtot = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    be._lib.check(be.L.wb_profile_steps(be.h, 5, ctypes.byref(md), ctypes.byref(mst),
+                                        ctypes.byref(mtot)), "wb_profile_steps")
+    tf = ctypes.c_double()
+    be._lib.check(be.L.wb_fp64_peak(dev, ctypes.byref(tf)), "wb_fp64_peak")
+    F = flops_per_step(be.n_fluid, n2, ex, ey)
+    fp64 = F / (mst.value * 1e-3) / 1e12
+    # end to end through the slab API with host buffers: upload each rank's
+    # columns (pinned), K steps, download the owned columns; max over ranks
+    q_host = torch.empty(sc.q0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    q_host[...] = sc.q0
+    del sim, be
+    torch.cuda.empty_cache()
+    dist.barrier()
+    t0 = time.perf_counter()
+    be2 = DeviceSlab(sc.grid, sc.params, q_host, lo, sc.boundary, 0.45, i0, i1, dev)
+    sim2 = DistributedSimulation(be2, sc.grid)
+    sim2.run_steps(args.steps, check_every=args.steps)
+    out = be2.owned_state()
+    wall = allmax(time.perf_counter() - t0)
+    if rank == 0:
+        state_bytes = sc.q0.nbytes * world
+        roof = {"bound": "fp64", "achieved": fp64, "peak": tf.value, "unit": "TFLOP/s",
+                "frac": fp64 / tf.value, "traffic": None,
+                "kernel": "k_step on rank 0's slab, timed alone (wb_profile_steps)",
+                "kernel_ms": mst.value, "flop_per_step": F,
+                "counters": {"n_second_order": n2, "x_faces": ex, "y_faces": ey,
+                             "n_fluid": be2.n_fluid}}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PUBLISHED,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "wall-impact (C5) dambreak, x-slab 4096x16384 per GPU",
+                           "grid": [nx, ny], "fluid_cells": n_fluid,
+                           "parallelism": f"x-slab dp{world}, {backend} halo send/recv + one "
+                                          "MAX all-reduce per step",
+                           "l2": "state 4.3 GB per GPU >> 126 MB L2 (no flush needed)"},
+                # per step: set_run, reset_counters, k_step, prefinalize, finalize,
+                # pack_halo, unpack_halo
+                "gpu_launches": 7 * args.steps,
+                "roofline": roof, "cpu_baseline": None,
+                "e2e": {"value": n_fluid * args.steps / wall, "unit": UNIT,
+                        "h2d_bytes_per_step": state_bytes / args.steps,
+                        "d2h_bytes_per_step": out.nbytes * world / args.steps,
+                        "api": "DeviceSlab(q host) -> DistributedSimulation.run_steps(K) -> "
+                               "owned_state() (host), max over ranks"},
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 def ctypes_void(p):
     import ctypes

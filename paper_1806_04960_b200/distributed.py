@@ -31,7 +31,7 @@ import numpy as np
 
 from .errors import SimulationError
 
-__all__ = ["slab_bounds", "DeviceSlab", "DistributedSimulation", "run_bench_distributed"]
+__all__ = ["slab_bounds", "stored_range", "DeviceSlab", "DistributedSimulation"]
 
 HALO = 2
 ENC_TOP = 1 << 62
@@ -313,79 +313,3 @@ class DistributedSimulation:
             if max_steps is not None and self.step_count >= max_steps:
                 break
         return self.t
-
-
-def run_bench_distributed(args):
-    """bench.py body for N > 1 ranks (torchrun): wall-impact, one 4096 x 16384
-    x-slab per GPU, global grid (4096 N) x 16384 (weak scaling); device time
-    of K steps is the max over ranks."""
-    import json
-    import torch
-    import torch.distributed as dist
-    from .scenarios import build_scenario
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    import time
-    nx, ny = 4096 * world, 16384
-    i0, i1 = slab_bounds(nx, world, rank)
-    lo, hi = stored_range(nx, i0, i1)
-    sc = build_scenario("wall-impact", (nx, ny), columns=(lo, hi))
-    grid = sc.grid
-    be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, local)
-    sim = DistributedSimulation(be, sc.grid)
-    sim.run_steps(args.warmup)
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(be.stream)
-    for _ in range(args.steps):
-        sim._enqueue_step()
-    e1.record(be.stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    s = sim._sync()
-    sim._check(s)
-    ms = float(ms.item())
-    n_fluid = int(np.count_nonzero(np.asarray(grid.mask)))
-    value = n_fluid * args.steps / (ms * 1e-3)
-    # end to end through the slab API with host buffers: upload each rank's
-    # columns (pinned), K steps, download the owned columns; max over ranks
-    q_host = torch.empty(sc.q0.shape, dtype=torch.float64, pin_memory=True).numpy()
-    q_host[...] = sc.q0
-    dist.barrier()
-    t0 = time.perf_counter()
-    be2 = DeviceSlab(sc.grid, sc.params, q_host, lo, sc.boundary, 0.45, i0, i1, local)
-    sim2 = DistributedSimulation(be2, sc.grid)
-    sim2.run_steps(args.steps, check_every=args.steps)
-    out = be2.owned_state()
-    wall = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
-                        device=f"cuda:{local}")
-    dist.all_reduce(wall, op=dist.ReduceOp.MAX)
-    wall = float(wall.item())
-    if rank == 0:
-        state_bytes = sc.q0.nbytes * world
-        line = {"metric": "FP64 cell updates/sec at 1/2/4/8 B200; % of HBM/FP64 roofline; "
-                          "CPU baseline",
-                "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": value / 2.0e7, "dtype": "f64",
-                "data": "synthetic",
-                "config": {"workload": "wall-impact (C5) dambreak, x-slab 4096x16384 per GPU",
-                           "grid": [nx, ny], "fluid_cells": n_fluid,
-                           "parallelism": f"x-slab dp{world}, NCCL halo send/recv + one MAX "
-                                          "allreduce per step",
-                           "l2": "state 4.3 GB per GPU >> L2"},
-                "gpu_launches": 6 * args.steps,
-                "roofline": None, "cpu_baseline": None,
-                "e2e": {"value": n_fluid * args.steps / wall, "unit": "cell-updates/s",
-                        "h2d_bytes_per_step": state_bytes / args.steps,
-                        "d2h_bytes_per_step": out.nbytes * world / args.steps,
-                        "api": "DeviceSlab(q host) -> DistributedSimulation.run_steps(K) -> "
-                               "owned_state() (host), max over ranks"}}
-        print(json.dumps(line), flush=True)
-    dist.destroy_process_group()
