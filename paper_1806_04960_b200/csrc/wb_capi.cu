@@ -376,11 +376,13 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   if (const char* v = getenv("WB_KSTEP_VARIANT")) h->variant = atoi(v);
   static const int nts[10] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64};
   const int nt = (h->variant >= 0 && h->variant < 10) ? nts[h->variant] : 64;
-  // keep at least ~4 CTAs per SM on small grids
+  // keep at least ~4 CTAs per SM on small grids: a CTA marches its rows
+  // sequentially, so on a small grid the step time is the row latency times
+  // the rows per CTA (C1 200x100: 0.093 ms/step at 8 rows, 0.055 at 2)
   int bx = (G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO);
   if (const char* v = getenv("WB_ROWS")) L = atoi(v);
   else if (cfg->rows_per_block <= 0)
-    while (L > 8 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
+    while (L > 2 && (long long)bx * ((G.ny + L - 1) / L) < 148 * 4) L /= 2;
   if (L > 64) L = 64;  // the fused detection keeps one fluid bit per row
   h->L = L;
   {
