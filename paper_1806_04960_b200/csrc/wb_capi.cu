@@ -105,7 +105,7 @@ struct wb_handle {
   long long step = 0;
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
-  int variant = 0;  // k_step launch configuration (WB_KSTEP_VARIANT, experiments)
+  int variant = 0;  // k_step launch configuration (auto, or WB_KSTEP_VARIANT)
 };
 
 static int ensure_tmp(wb_handle* h, size_t bytes) {
@@ -373,7 +373,15 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   B.dtlog_cap = DTLOG_CAP;
 
   int L = cfg->rows_per_block > 0 ? cfg->rows_per_block : 64;
-  if (const char* v = getenv("WB_KSTEP_VARIANT")) h->variant = atoi(v);
+  if (const char* v = getenv("WB_KSTEP_VARIANT")) {
+    h->variant = atoi(v);
+  } else {
+    // 128-thread CTAs (124 owned columns) halve the redundant halo columns of
+    // the 64-thread ones (9.69 vs 9.89 ms on the C5 slab) once the grid is
+    // large enough to keep 4 such CTAs per SM busy at 64 rows per CTA
+    const long long ctas128 = (long long)((G.nxl + 123) / 124) * ((G.ny + 63) / 64);
+    h->variant = ctas128 >= 148 * 4 ? 6 : 0;
+  }
   static const int nts[10] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64};
   const int nt = (h->variant >= 0 && h->variant < 10) ? nts[h->variant] : 64;
   // keep at least ~4 CTAs per SM on small grids: a CTA marches its rows

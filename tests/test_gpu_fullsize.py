@@ -46,7 +46,7 @@ def test_c5_launch_variants_equal(torch_cuda, monkeypatch):
     from paper_1806_04960_b200.timestepper import Simulation
     sc = build_scenario("wall-impact", (4096, 16384))
     out = []
-    for v in ("0", "3", "7"):
+    for v in ("0", "6", "3", "7"):
         monkeypatch.setenv("WB_KSTEP_VARIANT", v)
         sim = Simulation(sc.grid, sc.params, sc.q0, sc.boundary)
         sim.run_steps(3)
