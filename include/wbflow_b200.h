@@ -146,6 +146,20 @@ int wb_pack_halo(wb_handle* h, void* send_dev);
 int wb_unpack_halo(wb_handle* h, const void* recv_dev, int32_t have_left, int32_t have_right);
 int wb_sync(wb_handle* h);
 
+/* Overlapped step (SURVEY.md 8(e) "Overlap"; replaces the same
+ * Simulation.advance, timestepper.py:163-218): the two slab-edge column
+ * strips run on the edge stream and their new boundary columns are packed
+ * into send_dev while the interior strips run on the handle's stream.
+ *   wb_step_begin -> [exchange send/recv on the edge stream]
+ *   -> wb_unpack_halo_next -> wb_step_end -> all-reduce -> wb_finalize
+ * The halo lands in the step's output buffer, so it is committed (or
+ * discarded) together with the step. */
+int wb_set_edge_stream(wb_handle* h, void* cuda_stream);
+int wb_step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void* send_dev);
+int wb_unpack_halo_next(wb_handle* h, const void* recv_dev, int32_t have_left,
+                        int32_t have_right);
+int wb_step_end(wb_handle* h);
+
 /* ---- measurement ---- */
 /* n steps launched one by one with CUDA events on the handle's stream:
  * average device time of the detection kernel, the fused step kernel and the

@@ -312,6 +312,7 @@ class OracleSlab:
         self.err = (0, None, 0, 0.0)
         self.key_prep = None
         self.dt = 0.0
+        self.qn = None
 
     # owned columns in local indexing
     def _owned(self):
@@ -356,6 +357,7 @@ class OracleSlab:
     def step_local(self, max_dt, t_end, mode):
         key_r = key_u = None
         rnext = 0.0
+        self.qn = None
         if not self.stop and np.isfinite(self.rmax) and self.rmax > 0.0:
             dt = self.cfl / self.rmax
             if mode == 1:
@@ -433,11 +435,26 @@ class OracleSlab:
             return [self.i0 + h - self.lo for h in range(H)]
         return [self.i1 - H + h - self.lo for h in range(H)]
 
-    def pack_halo(self):
+    # overlapped step (k_step edge/interior launches, wb_step_begin/_end): the
+    # halo moves between the step's output states before the commit
+    def step_begin(self, max_dt, t_end, mode):
+        self.step_local(max_dt, t_end, mode)
+        self.pack_halo(next_buf=True)
+
+    def unpack_halo_next(self, have_left, have_right):
+        self.unpack_halo(have_left, have_right, next_buf=True)
+
+    def step_end(self):
+        pass
+
+    def pack_halo(self, next_buf=False):
         """Same layout as the device: per side, 4 x HALO x ny state values and
         then (y0, aeq) per halo column (the oracle recomputes detection itself,
         so those two slots are filled with the column's detection but unused)."""
         if self.stop > 0:
+            return
+        q = self.qn if next_buf else self.q
+        if q is None:  # no step was computed (non-finite rate): nothing to send
             return
         H, ny = self.HALO, self.ny
         blk = 4 * H * ny + 2 * H
@@ -445,13 +462,16 @@ class OracleSlab:
         for side in range(2):
             st = np.zeros((4, H, ny))
             for h, c in enumerate(self._halo_cols(side)):
-                if 0 <= c < self.q.shape[0]:
-                    st[:, h, :] = self.q[c, :, :4].T
+                if 0 <= c < q.shape[0]:
+                    st[:, h, :] = q[c, :, :4].T
             buf[side, :4 * H * ny] = st.ravel()
         self.send.copy_(__import__("torch").from_numpy(buf.ravel()))
 
-    def unpack_halo(self, have_left, have_right):
+    def unpack_halo(self, have_left, have_right, next_buf=False):
         if self.stop > 0:
+            return
+        q = self.qn if next_buf else self.q
+        if q is None:
             return
         H, ny = self.HALO, self.ny
         blk = 4 * H * ny + 2 * H
@@ -459,11 +479,11 @@ class OracleSlab:
         if have_left:
             st = buf[0, :4 * H * ny].reshape(4, H, ny)
             for h in range(H):
-                self.q[self.i0 - H + h - self.lo, :, :4] = st[:, h, :].T
+                q[self.i0 - H + h - self.lo, :, :4] = st[:, h, :].T
         if have_right:
             st = buf[1, :4 * H * ny].reshape(4, H, ny)
             for h in range(H):
-                self.q[self.i1 + h - self.lo, :, :4] = st[:, h, :].T
+                q[self.i1 + h - self.lo, :, :4] = st[:, h, :].T
 
     def status(self):
         return {"t": self.t, "dt": self.dt, "step": self.step, "stop": self.stop,

@@ -88,6 +88,10 @@ SIGNATURES = {
     "wb_halo_count": [_H, ctypes.POINTER(ctypes.c_int64)],
     "wb_pack_halo": [_H, _V],
     "wb_unpack_halo": [_H, _V, ctypes.c_int32, ctypes.c_int32],
+    "wb_set_edge_stream": [_H, _V],
+    "wb_step_begin": [_H, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _V],
+    "wb_unpack_halo_next": [_H, _V, ctypes.c_int32, ctypes.c_int32],
+    "wb_step_end": [_H],
     "wb_sync": [_H],
     "wb_profile_steps": [_H, ctypes.c_int32, c_double_p, c_double_p, c_double_p],
     "wb_fp64_peak": [ctypes.c_int32, c_double_p],

@@ -82,6 +82,8 @@ struct wb_handle {
   int L = 64;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t edge = nullptr;  // slab-edge strips + halo exchange (wb_set_edge_stream)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* planes = nullptr;
   uint8_t* mask = nullptr;
   double *y0s = nullptr, *aeqs = nullptr, *ycent = nullptr, *yfaces = nullptr,
@@ -144,30 +146,59 @@ static dim3 step_grid(const wb_handle* h, int nt) {
   return dim3((h->G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO), (h->G.ny + h->L - 1) / h->L);
 }
 
+// CTA width of each launch variant (WB_KSTEP_VARIANT)
+static const int kVariantNT[10] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64};
+static int step_nt(const wb_handle* h, bool debug) {
+  if (!h->g1 || debug) return 64;
+  return (h->variant >= 0 && h->variant < 10) ? kVariantNT[h->variant] : 64;
+}
+
+// Which column strips of the step grid a launch covers: all of them, only the
+// two slab-edge strips (they produce the columns the x-neighbours need), or
+// the interior strips (run concurrently with the edge strips' halo exchange).
+enum { PART_ALL = 0, PART_EDGE = 1, PART_INTERIOR = 2 };
+
 template <bool DEBUG>
-static void launch_step(wb_handle* h, const Dbg& D) {
+static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
+                        int which = PART_ALL) {
+  if (!s) s = h->stream;
   const Geo& G = h->G;
+  const int nt = step_nt(h, DEBUG);
+  dim3 g = step_grid(h, nt);
+  Part part{0, 1, 0};
+  // the edge launch must produce both halo-source column pairs: split only if
+  // there is an interior strip and the last strip owns at least HALO columns
+  const bool split = g.x >= 3 && h->G.nxl - ((int)g.x - 1) * (nt - 2 * HALO) >= HALO;
+  if (which == PART_EDGE) {
+    part = split ? Part{0, (int)g.x - 1, 1} : Part{0, 1, 1};
+    if (split) g.x = 2;
+  } else if (which == PART_INTERIOR) {
+    if (!split) return;
+    part = Part{1, 1, 0};
+    g.x -= 2;
+  }
+#define WB_LAUNCH(K, NTV) K<<<g, NTV, 0, s>>>(G, h->B, h->P, h->L, D, part)
   if (!h->g1) {
-    k_step<64, 1, false, DEBUG><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
+    WB_LAUNCH((k_step<64, 1, false, DEBUG>), 64);
     return;
   }
   if (DEBUG) {
-    k_step<64, 1, true, true><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
+    WB_LAUNCH((k_step<64, 1, true, true>), 64);
     return;
   }
   switch (h->variant) {
-    case 1: k_step<64, 6, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 2: k_step<64, 8, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 3: k_step<128, 3, true, false><<<step_grid(h, 128), 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 4: k_step<128, 4, true, false><<<step_grid(h, 128), 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 5: k_step<32, 12, true, false><<<step_grid(h, 32), 32, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 6: k_step<128, 2, true, false><<<step_grid(h, 128), 128, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 7: k_step<96, 4, true, false><<<step_grid(h, 96), 96, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 8: k_step_r<64, 200, true><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-    case 9: k_step_r<64, 224, true><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D); break;
-
-    default: k_step<64, 1, true, false><<<step_grid(h, 64), 64, 0, h->stream>>>(G, h->B, h->P, h->L, D);
+    case 1: WB_LAUNCH((k_step<64, 6, true, false>), 64); break;
+    case 2: WB_LAUNCH((k_step<64, 8, true, false>), 64); break;
+    case 3: WB_LAUNCH((k_step<128, 3, true, false>), 128); break;
+    case 4: WB_LAUNCH((k_step<128, 4, true, false>), 128); break;
+    case 5: WB_LAUNCH((k_step<32, 12, true, false>), 32); break;
+    case 6: WB_LAUNCH((k_step<128, 2, true, false>), 128); break;
+    case 7: WB_LAUNCH((k_step<96, 4, true, false>), 96); break;
+    case 8: WB_LAUNCH((k_step_r<64, 200, true>), 64); break;
+    case 9: WB_LAUNCH((k_step_r<64, 224, true>), 64); break;
+    default: WB_LAUNCH((k_step<64, 1, true, false>), 64);
   }
+#undef WB_LAUNCH
 }
 
 static void launch_detect(wb_handle* h) {
@@ -382,8 +413,7 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
     const long long ctas128 = (long long)((G.nxl + 123) / 124) * ((G.ny + 63) / 64);
     h->variant = ctas128 >= 148 * 4 ? 6 : 0;
   }
-  static const int nts[10] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64};
-  const int nt = (h->variant >= 0 && h->variant < 10) ? nts[h->variant] : 64;
+  const int nt = (h->variant >= 0 && h->variant < 10) ? kVariantNT[h->variant] : 64;
   // keep at least ~4 CTAs per SM on small grids: a CTA marches its rows
   // sequentially, so on a small grid the step time is the row latency times
   // the rows per CTA (C1 200x100: 0.093 ms/step at 8 rows, 0.055 at 2)
@@ -439,6 +469,8 @@ int wb_destroy(wb_handle* h) {
   cudaFree(h->scratch);
   if (h->tmp) cudaFree(h->tmp);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
   return WB_OK;
 }
@@ -853,14 +885,67 @@ int wb_halo_count(wb_handle* h, int64_t* n) {
 int wb_pack_halo(wb_handle* h, void* send) {
   if (!h || !send) return WB_E_ARG;
   CK(cudaSetDevice(h->dev));
-  k_pack_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, (double*)send);
+  k_pack_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, (double*)send, 0);
   CK(cudaGetLastError());
   return WB_OK;
 }
 int wb_unpack_halo(wb_handle* h, const void* recv, int32_t hl, int32_t hr) {
   if (!h || !recv) return WB_E_ARG;
   CK(cudaSetDevice(h->dev));
-  k_unpack_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, (const double*)recv, hl, hr);
+  k_unpack_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, (const double*)recv, hl, hr, 0);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+
+// ---- overlapped multi-GPU step (SURVEY.md 8(e) "Overlap") ----
+int wb_set_edge_stream(wb_handle* h, void* s) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->edge) CK(cudaStreamSynchronize(h->edge));
+  h->edge = (cudaStream_t)s;
+  if (!h->ev_fork) CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  if (!h->ev_join) CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  return WB_OK;
+}
+// Stream s: set_run, [detect], reset_counters, then the interior strips.
+// Edge stream: after the reset, the two slab-edge strips, then the pack of
+// their new halo-source columns (from the step's output buffer) into `send`.
+// The caller exchanges `send`/`recv` on the edge stream, calls
+// wb_unpack_halo_next there, then wb_step_end.
+int wb_step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void* send) {
+  if (!h || !send) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  if (!h->edge) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  int has = !isnan(max_dt);
+  double tiny = mode ? 1.0e-12 * std::max(1.0, fabs(t_end)) : 0.0;
+  k_set_run<<<1, 1, 0, h->stream>>>(h->st, mode, has, has ? max_dt : 0.0, t_end, tiny, -1, 0);
+  if (!h->B.fuse_detect) launch_detect(h);
+  k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
+  CK(cudaEventRecord(h->ev_fork, h->stream));
+  CK(cudaStreamWaitEvent(h->edge, h->ev_fork, 0));
+  launch_step<false>(h, Dbg{}, h->edge, PART_EDGE);
+  k_pack_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, (double*)send, 1);
+  launch_step<false>(h, Dbg{}, h->stream, PART_INTERIOR);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_unpack_halo_next(wb_handle* h, const void* recv, int32_t hl, int32_t hr) {
+  if (!h || !recv || !h->edge) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  k_unpack_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, (const double*)recv, hl, hr, 1);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+// Join the edge stream into s and prepare the reduction vector (then the
+// caller all-reduces it on s and calls wb_finalize).
+int wb_step_end(wb_handle* h) {
+  if (!h || !h->edge) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  CK(cudaEventRecord(h->ev_join, h->edge));
+  CK(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  k_prefinalize<<<1, 1, 0, h->stream>>>(h->st);
   CK(cudaGetLastError());
   return WB_OK;
 }

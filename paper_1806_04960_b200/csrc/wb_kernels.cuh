@@ -31,8 +31,7 @@ struct Status {
   double err_rmax;
   unsigned long long rmax_used_bits;  // rate the last committed step used for dt
   unsigned long long launch_id;       // incremented before every step launch
-  unsigned int ticket;                // dynamic CTA index of the step kernel
-  unsigned int pad2;
+  unsigned int ticket[2];  // dynamic CTA index of the step kernel, per concurrent launch
 };
 
 struct Geo {
@@ -70,6 +69,12 @@ struct Bufs {
 };
 
 // Debug outputs in the reference layout (owned columns, (nxl, ny, 5))
+// Column-strip partition of one step launch: launch-local strip k is global
+// strip bx0 + k*bxs; tslot picks the ticket counter (two launches of one step
+// -- slab-edge strips and interior strips -- run concurrently)
+struct Part {
+  int bx0, bxs, tslot;
+};
 struct Dbg {
   double *fW, *fE, *fS, *fN, *vol, *psi, *DW, *DE, *DS, *DN;
   uint8_t* quiet;

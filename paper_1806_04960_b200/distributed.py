@@ -91,6 +91,11 @@ class DeviceSlab:
         self.stream = torch.cuda.Stream(device=device)
         _lib.check(self.L.wb_set_stream(h, ctypes.c_void_p(self.stream.cuda_stream)),
                    "wb_set_stream")
+        # slab-edge strips + halo exchange (overlapped step); high priority so
+        # the boundary columns are done early and the exchange starts early
+        self.edge_stream = torch.cuda.Stream(device=device, priority=-1)
+        _lib.check(self.L.wb_set_edge_stream(h, ctypes.c_void_p(self.edge_stream.cuda_stream)),
+                   "wb_set_edge_stream")
         q = np.ascontiguousarray(q_cols, dtype=np.float64)
         bi, bj = ctypes.c_int32(), ctypes.c_int32()
         _lib.check(self.L.wb_set_state(h, q.ctypes.data_as(ctypes.c_void_p), col0, q.shape[0],
@@ -106,6 +111,23 @@ class DeviceSlab:
 
     def stream_ctx(self):
         return self.torch.cuda.stream(self.stream)
+
+    def edge_ctx(self):
+        return self.torch.cuda.stream(self.edge_stream)
+
+    def step_begin(self, max_dt, t_end, mode):
+        self._lib.check(self.L.wb_step_begin(self.h, math.nan if max_dt is None else max_dt,
+                                             0.0 if t_end is None else t_end, mode,
+                                             ctypes.c_void_p(self.send.data_ptr())),
+                        "wb_step_begin")
+
+    def unpack_halo_next(self, have_left, have_right):
+        self._lib.check(self.L.wb_unpack_halo_next(self.h, ctypes.c_void_p(self.recv.data_ptr()),
+                                                   int(have_left), int(have_right)),
+                        "wb_unpack_halo_next")
+
+    def step_end(self):
+        self._lib.check(self.L.wb_step_end(self.h), "wb_step_end")
 
     def prepare_local(self):
         self._lib.check(self.L.wb_prepare_local(self.h), "wb_prepare_local")
@@ -174,7 +196,7 @@ class DistributedSimulation:
     torch.distributed process group (the reference's Simulation semantics:
     same dt sequence, same error step/cell, bit-identical state)."""
 
-    def __init__(self, backend, grid, cfl=0.45, group=None):
+    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=False):
         import torch.distributed as dist
         self.dist = dist
         self.be = backend
@@ -187,6 +209,13 @@ class DistributedSimulation:
         self.step_count = 0
         self._prepared = False
         self._nccl = dist.get_backend(group) == "nccl"
+        # overlapped step: edge strips + halo exchange on the backend's edge
+        # stream while the interior strips run (SURVEY.md 8(e) "Overlap").
+        # Off by default: measured on one B200 (tools/overlap_bench.py, C5
+        # slab) the split costs ~0.5 ms per step -- the edge launch's fused
+        # detection chain runs its 256 row segments back to back -- against
+        # ~0.05 ms of exchange it could hide.
+        self.overlap = overlap and hasattr(backend, "step_begin")
 
     # -- collectives ------------------------------------------------------
     def _allreduce_max(self, t):
@@ -198,8 +227,14 @@ class DistributedSimulation:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
 
     def _halo_exchange(self):
+        self.be.pack_halo()
+        self._p2p()
+        self.be.unpack_halo(self.rank > 0, self.rank < self.world - 1)
+
+    def _p2p(self):
+        """send/recv of the packed halo blocks with the x-neighbours on the
+        current stream (NCCL), or through host copies (gloo)."""
         be, r, W = self.be, self.rank, self.world
-        be.pack_halo()
         half = be.send.numel() // 2
         staged = be.send.is_cuda and not self._nccl  # gloo: point-to-point on host copies
         send, recv = (be.send.cpu(), be.recv.cpu()) if staged else (be.send, be.recv)
@@ -221,7 +256,6 @@ class DistributedSimulation:
                     q.wait()
         if staged:
             be.recv.copy_(recv)
-        be.unpack_halo(r > 0, r < W - 1)
 
     def _ctx(self):
         return self.be.stream_ctx() if hasattr(self.be, "stream_ctx") else \
@@ -247,8 +281,23 @@ class DistributedSimulation:
         return rmax
 
     # -- stepping -----------------------------------------------------------
+    def _edge_ctx(self):
+        return self.be.edge_ctx() if hasattr(self.be, "edge_ctx") else contextlib.nullcontext()
+
     def _enqueue_step(self, max_dt=None, t_end=None):
         be = self.be
+        mode = 1 if t_end is not None else 0
+        if self.overlap:
+            with self._ctx():
+                be.step_begin(max_dt, t_end, mode)  # interior here, edges + pack on edge
+            with self._edge_ctx():
+                self._p2p()
+                be.unpack_halo_next(self.rank > 0, self.rank < self.world - 1)
+            with self._ctx():
+                be.step_end()                       # join the edge stream
+                self._allreduce_max(be.red)
+                be.finalize()
+            return
         with self._ctx():
             be.step_local(max_dt, t_end, 1 if t_end is not None else 0)
             self._allreduce_max(be.red)

@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, scen, res, steps, out, run_until):
+def _worker(rank, world, port, scen, res, steps, out, run_until, overlap=False):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
     import torch.distributed as dist
     import oracle as orc
@@ -40,7 +40,7 @@ def _worker(rank, world, port, scen, res, steps, out, run_until):
     lo, hi = stored_range(nx, i0, i1)
     sc = build_scenario(scen, res, columns=(lo, hi))
     be = orc.OracleSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1)
-    sim = DistributedSimulation(be, sc.grid)
+    sim = DistributedSimulation(be, sc.grid, overlap=overlap)
     err = None
     try:
         if run_until is not None:
@@ -55,9 +55,9 @@ def _worker(rank, world, port, scen, res, steps, out, run_until):
     dist.destroy_process_group()
 
 
-def _run(world, scen, res, steps=None, run_until=None):
+def _run(world, scen, res, steps=None, run_until=None, overlap=False):
     out = tempfile.mkdtemp()
-    mp.spawn(_worker, args=(world, _free_port(), scen, res, steps, out, run_until),
+    mp.spawn(_worker, args=(world, _free_port(), scen, res, steps, out, run_until, overlap),
              nprocs=world, join=True)
     parts = [np.load(os.path.join(out, f"rank{r}.npz")) for r in range(world)]
     q = np.concatenate([p["q"] for p in parts], axis=0)
@@ -79,9 +79,9 @@ def _reference(oracle, scen, res, steps=None, run_until=None):
     return sim, err
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slabs_bitexact(oracle, world):
-    q, parts = _run(world, "wall-impact", (61, 32), steps=12)
+@pytest.mark.parametrize("world,overlap", [(2, False), (3, False), (2, True), (3, True)])
+def test_slabs_bitexact(oracle, world, overlap):
+    q, parts = _run(world, "wall-impact", (61, 32), steps=12, overlap=overlap)
     ref, err = _reference(oracle, "wall-impact", (61, 32), steps=12)
     assert err is None
     assert np.array_equal(q, ref.q)

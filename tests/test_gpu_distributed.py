@@ -18,7 +18,8 @@ def _port():
     return p
 
 
-def test_nccl_world1_matches_simulation():
+@pytest.mark.parametrize("overlap", [False, True])
+def test_nccl_world1_matches_simulation(overlap):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -35,7 +36,7 @@ def test_nccl_world1_matches_simulation():
         lo, hi = stored_range(res[0], i0, i1)
         sc = build_scenario("wall-impact", res, columns=(lo, hi))
         be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
-        dsim = DistributedSimulation(be, sc.grid)
+        dsim = DistributedSimulation(be, sc.grid, overlap=overlap)
         dsim.run_steps(25, check_every=8)
         full = build_scenario("wall-impact", res)
         sim = Simulation(full.grid, full.params, full.q0, full.boundary)
@@ -50,7 +51,7 @@ def test_nccl_world1_matches_simulation():
         dist.destroy_process_group()
 
 
-def _gloo_worker(rank, world, port, scen, res, steps, out):
+def _gloo_worker(rank, world, port, scen, res, steps, out, overlap):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch.distributed as dist
@@ -64,7 +65,7 @@ def _gloo_worker(rank, world, port, scen, res, steps, out):
     lo, hi = stored_range(res[0], i0, i1)
     sc = build_scenario(scen, res, columns=(lo, hi))
     be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
-    dsim = DistributedSimulation(be, sc.grid)
+    dsim = DistributedSimulation(be, sc.grid, overlap=overlap)
     err = None
     try:
         dsim.run_steps(steps, check_every=7)
@@ -76,9 +77,10 @@ def _gloo_worker(rank, world, port, scen, res, steps, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scen,res,steps", [("wall-impact", (300, 160), 25),
-                                            ("dambreak-dry", (200, 100), 400)])
-def test_device_slabs_two_processes_gloo(scen, res, steps):
+@pytest.mark.parametrize("scen,res,steps,overlap", [("wall-impact", (300, 160), 25, True),
+                                                    ("wall-impact", (300, 160), 25, False),
+                                                    ("dambreak-dry", (200, 100), 400, True)])
+def test_device_slabs_two_processes_gloo(scen, res, steps, overlap):
     """The full multi-process driver (torch.distributed, two ranks, device
     slabs on cuda:0, collectives staged through host memory by gloo) against
     the single-handle Simulation: same state, t and step; on the dry dambreak
@@ -92,7 +94,8 @@ def test_device_slabs_two_processes_gloo(scen, res, steps):
     from paper_1806_04960_b200.scenarios import build_scenario
     from paper_1806_04960_b200.timestepper import Simulation
     out = tempfile.mkdtemp()
-    mp.spawn(_gloo_worker, args=(2, _port(), scen, res, steps, out), nprocs=2, join=True)
+    mp.spawn(_gloo_worker, args=(2, _port(), scen, res, steps, out, overlap), nprocs=2,
+             join=True)
     parts = [np.load(os.path.join(out, f"rank{r}.npz")) for r in range(2)]
     full = build_scenario(scen, res)
     sim = Simulation(full.grid, full.params, full.q0, full.boundary)

@@ -24,13 +24,14 @@ def torch_cuda():
     return torch
 
 
-def test_c4_weir_slabs_equal_single(torch_cuda):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_c4_weir_slabs_equal_single(torch_cuda, overlap):
     from test_gpu_slabs import _run, _slabs
     from paper_1806_04960_b200.scenarios import build_scenario
     from paper_1806_04960_b200.timestepper import Simulation
     res = (16384, 8192)
     slabs = _slabs(torch_cuda, "weir", res, 3)
-    assert _run(torch_cuda, slabs, 4) is None
+    assert _run(torch_cuda, slabs, 4, overlap=overlap) is None
     q_slabs = np.concatenate([s.owned_state() for s in slabs], axis=0)
     t_slabs = slabs[0].status()["t"]
     del slabs

@@ -58,7 +58,24 @@ def _halo(torch, slabs):
     torch.cuda.synchronize()
 
 
-def _run(torch, slabs, steps):
+def _exchange(torch, slabs):
+    torch.cuda.synchronize()
+    W = len(slabs)
+    half = slabs[0].send.numel() // 2
+    for r, s in enumerate(slabs):
+        if r > 0:
+            s.recv[:half].copy_(slabs[r - 1].send[half:])
+        if r < W - 1:
+            s.recv[half:].copy_(slabs[r + 1].send[:half])
+    torch.cuda.synchronize()
+
+
+def _run(torch, slabs, steps, overlap=False):
+    """Drive the slabs like distributed.DistributedSimulation: either
+    step_local -> all-reduce -> finalize -> halo exchange, or the overlapped
+    step_begin (edge strips + pack on the edge stream, interior strips on the
+    main stream) -> exchange -> unpack_halo_next -> step_end -> all-reduce ->
+    finalize."""
     for s in slabs:
         s.prepare_local()
         s.prepare_pack()
@@ -67,13 +84,26 @@ def _run(torch, slabs, steps):
         s.prepare_unpack()
     for s in slabs:
         assert s.check_prepare()[1] == 0
+    W = len(slabs)
     for _ in range(steps):
-        for s in slabs:
-            s.step_local(None, None, 0)
-        _reduce(torch, slabs)
-        for s in slabs:
-            s.finalize()
-        _halo(torch, slabs)
+        if overlap:
+            for s in slabs:
+                s.step_begin(None, None, 0)
+            _exchange(torch, slabs)
+            for r, s in enumerate(slabs):
+                s.unpack_halo_next(r > 0, r < W - 1)
+            for s in slabs:
+                s.step_end()
+            _reduce(torch, slabs)
+            for s in slabs:
+                s.finalize()
+        else:
+            for s in slabs:
+                s.step_local(None, None, 0)
+            _reduce(torch, slabs)
+            for s in slabs:
+                s.finalize()
+            _halo(torch, slabs)
         st = [s.status() for s in slabs]
         if st[0]["stop"] > 0:
             return [s.last_error() for s in slabs]
@@ -97,6 +127,30 @@ def test_device_slabs_bitexact(torch_cuda, oracle, world):
 def test_device_slabs_error_stop(torch_cuda):
     slabs = _slabs(torch_cuda, "dambreak-dry", (200, 100), 2)
     errs = _run(torch_cuda, slabs, 400)
+    assert errs is not None
+    for code, key, step, _ in errs:
+        assert (code, divmod(key, 100), step) == (4, (98, 37), 309)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_slabs_overlapped_bitexact(torch_cuda, oracle, world):
+    """Overlapped step with a real edge/interior split (>= 3 column strips
+    per slab at 64-thread CTAs) against the oracle."""
+    from paper_1806_04960_b200.scenarios import build_scenario
+    res = (400 * world, 96)
+    slabs = _slabs(torch_cuda, "wall-impact", res, world)
+    assert _run(torch_cuda, slabs, 12, overlap=True) is None
+    q = np.concatenate([s.owned_state() for s in slabs], axis=0)
+    sc = build_scenario("wall-impact", res)
+    ref = oracle.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
+    ref.run_steps(12)
+    assert np.array_equal(q, ref.q)
+    assert all(s.status()["t"] == ref.t for s in slabs)
+
+
+def test_device_slabs_overlapped_error_stop(torch_cuda):
+    slabs = _slabs(torch_cuda, "dambreak-dry", (200, 100), 2)
+    errs = _run(torch_cuda, slabs, 400, overlap=True)
     assert errs is not None
     for code, key, step, _ in errs:
         assert (code, divmod(key, 100), step) == (4, (98, 37), 309)
