@@ -171,6 +171,13 @@ int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step
 int wb_selftest_div(int32_t device, int64_t n, uint64_t seed, uint64_t* mismatches);
 /* the device exp() used by eq_rho (glibc 2.39 restatement) on n host values */
 int wb_eval_exp(int32_t device, const double* x, double* y, int64_t n);
+/* face solvers on host arrays of state pairs (components 0..3 of each state;
+ * both at the same height, as in the time loop), with the handle's physics:
+ * kind 0 = osher_x_edge (kernels.py:215-271), kind 1 = or_y_edge
+ * (kernels.py:308-425) with aux = (y, y0, aeq) per pair.  dm/dp get D-/D+
+ * components 0..3 (component 4 is exactly 0).  For randomized parity tests. */
+int wb_eval_faces(wb_handle* h, int32_t kind, int64_t n, const double* qm, const double* qp,
+                  const double* aux, double* dm, double* dp);
 /* measured FP64 FMA throughput of the device (TFLOP/s, 2 flop per DFMA) */
 int wb_fp64_peak(int32_t device, double* tflops);
 

@@ -1065,6 +1065,32 @@ int wb_eval_exp(int32_t device, const double* x, double* y, int64_t n) {
   return WB_OK;
 }
 
+int wb_eval_faces(wb_handle* h, int32_t kind, int64_t n, const double* qm, const double* qp,
+                  const double* aux, double* dm, double* dp) {
+  if (!h || n <= 0 || !qm || !qp || !dm || !dp || (kind != 0 && kind != 1) ||
+      (kind == 1 && !aux))
+    return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamSynchronize(h->stream));
+  double* d;
+  const size_t na = kind == 1 ? 3 * (size_t)n : 1;
+  CK(cudaMalloc(&d, (16 * (size_t)n + na) * sizeof(double)));
+  double *dqm = d, *dqp = d + 4 * n, *ddm = d + 8 * n, *ddp = d + 12 * n, *dax = d + 16 * n;
+  CK(cudaMemcpy(dqm, qm, 4 * n * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dqp, qp, 4 * n * sizeof(double), cudaMemcpyHostToDevice));
+  if (kind == 1) CK(cudaMemcpy(dax, aux, 3 * n * sizeof(double), cudaMemcpyHostToDevice));
+  if (h->g1)
+    k_eval_faces<true><<<148 * 4, 128, 0, h->stream>>>(h->P, kind, n, dqm, dqp, dax, ddm, ddp);
+  else
+    k_eval_faces<false><<<148 * 4, 128, 0, h->stream>>>(h->P, kind, n, dqm, dqp, dax, ddm, ddp);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(dm, ddm, 4 * n * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(dp, ddp, 4 * n * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return WB_OK;
+}
+
 int wb_sync(wb_handle* h) {
   if (!h) return WB_E_ARG;
   int rc = read_status(h);

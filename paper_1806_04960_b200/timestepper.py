@@ -358,6 +358,28 @@ class Simulation:
         self._sync_time()
         return self._step
 
+    def eval_faces(self, kind, qm, qp, aux=None):
+        """The device face solvers on arrays of state pairs with this
+        simulation's physics (test hook, ``wb_eval_faces``): kind "x" =
+        osher_x_edge, kind "y" = or_y_edge with aux rows (y, y0, aeq).  qm, qp
+        are (n, 4); returns (D-, D+) as (n, 4) arrays."""
+        qm = np.ascontiguousarray(qm, dtype=np.float64)
+        qp = np.ascontiguousarray(qp, dtype=np.float64)
+        n = qm.shape[0]
+        if qm.shape != (n, 4) or qp.shape != (n, 4):
+            raise ValueError("qm and qp must have shape (n, 4)")
+        k = {"x": 0, "y": 1}[kind]
+        ax = None
+        if k == 1:
+            ax = np.ascontiguousarray(aux, dtype=np.float64)
+            if ax.shape != (n, 3):
+                raise ValueError("aux must have shape (n, 3): (y, y0, aeq)")
+        dm, dp = np.empty((n, 4)), np.empty((n, 4))
+        check(self._L.wb_eval_faces(self._h, k, n, dptr(qm), dptr(qp),
+                                    dptr(ax) if ax is not None else None, dptr(dm), dptr(dp)),
+              "wb_eval_faces")
+        return dm, dp
+
     def dt_log(self, n=None):
         n = self._step if n is None else n
         out = np.empty(n)
