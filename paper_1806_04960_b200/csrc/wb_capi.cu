@@ -110,6 +110,14 @@ struct wb_handle {
   int variant = 0;  // k_step launch configuration (auto, or WB_KSTEP_VARIANT)
 };
 
+// columns per host-transfer chunk: ~128 MB of AoS, a multiple of the
+// transpose tile
+static int chunk_cols(int ny) {
+  long long c = (128LL << 20) / ((long long)ny * 5 * sizeof(double));
+  c = std::max(32LL, c / TT * TT);
+  return (int)c;
+}
+
 static int ensure_tmp(wb_handle* h, size_t bytes) {
   if (h->tmp_bytes >= bytes) return WB_OK;
   if (h->tmp) cudaFree(h->tmp);
@@ -499,17 +507,26 @@ int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
     return WB_E_ARG;
   }
   CK(cudaSetDevice(h->dev));
-  const size_t bytes = (size_t)n_cols * G.ny * 5 * sizeof(double);
-  const double* src = q;
-  if (!is_device) {
-    int rc = ensure_tmp(h, bytes);
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(h->tmp, q, bytes, cudaMemcpyHostToDevice, h->stream));
-    src = h->tmp;
-  }
   CK(cudaMemsetAsync(h->scratch, 0xff, sizeof(unsigned long long), h->stream));
-  k_aos_to_planes<<<dim3((n_cols + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
-      h->G, h->B, src, i_first, n_cols, h->scratch);
+  if (is_device) {
+    k_aos_to_planes<<<dim3((n_cols + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0,
+                      h->stream>>>(h->G, h->B, q, i_first, n_cols, h->scratch);
+  } else {
+    // host source: column chunks through one device staging buffer (stream
+    // order makes the reuse safe), so an upload needs ~128 MB of scratch
+    // instead of a full 40 B/cell AoS copy on the device
+    const int ch = chunk_cols(G.ny);
+    int rc = ensure_tmp(h, (size_t)ch * G.ny * 5 * sizeof(double));
+    if (rc) return rc;
+    for (int k = 0; k < n_cols; k += ch) {
+      const int nk = std::min(ch, n_cols - k);
+      CK(cudaMemcpyAsync(h->tmp, q + (size_t)k * G.ny * 5,
+                         (size_t)nk * G.ny * 5 * sizeof(double), cudaMemcpyHostToDevice,
+                         h->stream));
+      k_aos_to_planes<<<dim3((nk + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
+          h->G, h->B, h->tmp, i_first + k, nk, h->scratch);
+    }
+  }
   CK(cudaGetLastError());
   unsigned long long bad = 0;
   CK(cudaMemcpyAsync(&bad, h->scratch, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -535,17 +552,24 @@ int wb_get_state_buf(wb_handle* h, double* q, int32_t which, int32_t is_device) 
   if (!h || !q) return WB_E_ARG;
   if (!h->have_state) return WB_E_STATE;
   CK(cudaSetDevice(h->dev));
-  const size_t bytes = (size_t)h->G.nxl * h->G.ny * 5 * sizeof(double);
-  double* dst = q;
-  if (!is_device) {
-    int rc = ensure_tmp(h, bytes);
+  const Geo& G = h->G;
+  if (is_device) {
+    k_planes_to_aos<<<dim3((G.nxl + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
+        G, h->B, q, which ? 1 : -1, 0, G.nxl);
+  } else {
+    const int ch = chunk_cols(G.ny);
+    int rc = ensure_tmp(h, (size_t)ch * G.ny * 5 * sizeof(double));
     if (rc) return rc;
-    dst = h->tmp;
+    for (int k = 0; k < G.nxl; k += ch) {
+      const int nk = std::min(ch, G.nxl - k);
+      k_planes_to_aos<<<dim3((nk + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
+          G, h->B, h->tmp, which ? 1 : -1, k, nk);
+      CK(cudaMemcpyAsync(q + (size_t)k * G.ny * 5, h->tmp,
+                         (size_t)nk * G.ny * 5 * sizeof(double), cudaMemcpyDeviceToHost,
+                         h->stream));
+    }
   }
-  k_planes_to_aos<<<dim3((h->G.nxl + TT - 1) / TT, (h->G.ny + TT - 1) / TT), 256, 0,
-                    h->stream>>>(h->G, h->B, dst, which ? 1 : -1);
   CK(cudaGetLastError());
-  if (!is_device) CK(cudaMemcpyAsync(q, dst, bytes, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return WB_OK;
 }
