@@ -108,6 +108,10 @@ int wb_get_status(wb_handle* h, wb_status* s);
  * E_rho, E_u, E_v, E_P} where the E_* are max-norm errors against the exact
  * water-at-rest profile of surface level y0_eq (NaN skips) */
 int wb_diagnostics(wb_handle* h, double y0_eq, double* out9);
+/* depth-averaged velocity u_bar(x) = sum(u alpha dy) / sum(alpha dy) per
+ * owned column, fluid cells in j order (the reference has no
+ * such function) */
+int wb_depth_averaged_velocity(wb_handle* h, double* out_nx);
 /* the error that stopped the device-side run (code 0 if none) */
 int wb_get_error(wb_handle* h, wb_error* err);
 int wb_set_time(wb_handle* h, double t, int64_t step);

@@ -93,6 +93,7 @@ SIGNATURES = {
     "wb_unpack_halo_next": [_H, _V, ctypes.c_int32, ctypes.c_int32],
     "wb_step_end": [_H],
     "wb_eval_faces": [_H, ctypes.c_int32, ctypes.c_int64, _V, _V, _V, _V, _V],
+    "wb_depth_averaged_velocity": [_H, _V],
     "wb_sync": [_H],
     "wb_profile_steps": [_H, ctypes.c_int32, c_double_p, c_double_p, c_double_p],
     "wb_fp64_peak": [ctypes.c_int32, c_double_p],

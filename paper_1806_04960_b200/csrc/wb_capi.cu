@@ -767,6 +767,21 @@ int wb_diagnostics(wb_handle* h, double y0_eq, double* out9) {
   return WB_OK;
 }
 
+int wb_depth_averaged_velocity(wb_handle* h, double* out_host) {
+  if (!h || !out_host) return WB_E_ARG;
+  if (!h->have_state) return WB_E_STATE;
+  CK(cudaSetDevice(h->dev));
+  double* d;
+  CK(cudaMalloc(&d, (size_t)h->G.nxl * sizeof(double)));
+  k_depth_avg<<<(h->G.nxl + 127) / 128, 128, 0, h->stream>>>(h->G, h->B, h->P.dy, d);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_host, d, (size_t)h->G.nxl * sizeof(double), cudaMemcpyDeviceToHost,
+                     h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  cudaFree(d);
+  return WB_OK;
+}
+
 int wb_get_error(wb_handle* h, wb_error* err) {
   if (!h || !err) return WB_E_ARG;
   CK(cudaSetDevice(h->dev));

@@ -262,6 +262,14 @@ class Simulation:
                 d.pop(k)
         return d
 
+    def depth_averaged_velocity(self):
+        """u_bar(x) per column on the device (see analysis.depth_averaged_velocity
+        for the host formula; same terms, j-ordered sums)."""
+        out = np.empty(self.grid.nx)
+        check(self._L.wb_depth_averaged_velocity(self._h, dptr(out)),
+              "wb_depth_averaged_velocity")
+        return out
+
     # ---- errors -------------------------------------------------------------
     def _raise(self, e):
         if e.code == _lib.ERR_WAVE_SPEED:
