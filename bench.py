@@ -187,12 +187,16 @@ def run_ours(args):
     t_hbm = HBM_BYTES_PER_CELL * n_fluid / (hbm_peak * 1e9)
     t_fp64 = F / (tf.value * 1e12)
     traffic = None
+    ncu = None
     tpath = os.path.join(ROOT, "profiles", "kstep_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             tj = json.load(f)
         if tj.get("grid") == [nx, ny]:
             traffic = tj.get("dram_bytes_per_launch")
+            ncu = {k: tj.get(k) for k in ("fp64_pipe_active_pct", "issue_active_pct",
+                                           "warps_per_sm", "registers_per_thread")}
+            ncu["source"] = tj.get("source")
     roof = {"bound": "fp64" if t_fp64 >= t_hbm else "hbm",
             "achieved": fp64_achieved if t_fp64 >= t_hbm else hbm_achieved,
             "peak": tf.value if t_fp64 >= t_hbm else hbm_peak,
@@ -208,7 +212,10 @@ def run_ours(args):
                     "frac": hbm_achieved / hbm_peak,
                     "bytes_per_cell": HBM_BYTES_PER_CELL},
             "fp64": {"achieved": fp64_achieved, "peak": tf.value, "unit": "TFLOP/s",
-                     "frac": fp64_achieved / tf.value}}
+                     "frac": fp64_achieved / tf.value},
+            # hardware view of the same kernel from the committed ncu capture:
+            # exact IEEE divisions cost ~9 FP64-pipe instructions per flop
+            "ncu": ncu}
     roof["frac"] = roof["achieved"] / roof["peak"]
     # ---- end to end through the public API with host buffers ----
     q_host = torch.empty((nx, ny, 5), dtype=torch.float64, pin_memory=True).numpy()

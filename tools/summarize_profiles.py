@@ -37,8 +37,17 @@ unit = {k: u[i] for i, k in enumerate(h) if k in val}
 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
 rd = val["dram__bytes_read.sum"] * scale[unit["dram__bytes_read.sum"]]
 wr = val["dram__bytes_write.sum"] * scale[unit["dram__bytes_write.sum"]]
+def _metric(name):
+    return float(v[h.index(name)].replace(",", "")) if name in h else None
+
+
 json.dump({"grid": [4096, 16384], "kernel": "k_step", "dram_bytes_read": rd,
            "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+           "fp64_pipe_active_pct": _metric(
+               "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+           "issue_active_pct": _metric("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+           "warps_per_sm": _metric("sm__warps_active.avg.per_cycle_active"),
+           "registers_per_thread": _metric("launch__registers_per_thread"),
            "algorithmic_bytes_per_launch": 64.0 * 4096 * 16384,
            "source": f"ncu --set full -k regex:k_step -s 3 -c 1, round {rnd} "
                      f"(profiles/r{rnd}_kstep_ncu_raw_selected.csv)"},
