@@ -263,6 +263,9 @@ extern "C" {
 const char* wb_last_error(void) { return g_err.c_str(); }
 int wb_version(void) { return 1; }
 
+static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
+                       const double* xcent, const double* ycent, const double* yfaces);
+
 int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
               const double* ycent, const double* yfaces, wb_handle** out) {
   if (!cfg || !mask || !xcent || !ycent || !yfaces || !out) return WB_E_ARG;
@@ -273,6 +276,19 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
   }
   wb_handle* h = new wb_handle();
   h->dev = cfg->device;
+  const int rc = create_body(h, cfg, mask, xcent, ycent, yfaces);
+  if (rc != WB_OK) {  // e.g. out of device memory: release what was allocated
+    const std::string msg = g_err;
+    wb_destroy(h);
+    g_err = msg;
+    return rc;
+  }
+  *out = h;
+  return WB_OK;
+}
+
+static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
+                       const double* xcent, const double* ycent, const double* yfaces) {
   CK(cudaSetDevice(h->dev));
   static bool tab_done[64] = {false};
   if (h->dev < 64 && !tab_done[h->dev]) {
@@ -451,7 +467,6 @@ int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
     if (const char* v = getenv("WB_FUSE_DETECT")) h->B.fuse_detect = atoi(v) ? 1 : 0;
   }
   CK(cudaStreamSynchronize(h->stream));
-  *out = h;
   return WB_OK;
 }
 
