@@ -11,7 +11,9 @@ import os
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwbflow_b200.so")
+# WB_LIB_PATH: load another build of the same sources (measurement experiments
+# such as tools/exp_nocheck.sh); the default is the in-tree library
+LIB_PATH = os.environ.get("WB_LIB_PATH") or os.path.join(_HERE, "libwbflow_b200.so")
 
 WB_OK = 0
 WB_E_ARG, WB_E_CUDA, WB_E_HEIGHT, WB_E_STATE = -1, -2, -3, -4
