@@ -360,12 +360,13 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
     P.yrho0 = hv[0]; P.ycref = hv[1]; P.yc2c = hv[2]; P.ydx = hv[3]; P.ydy = hv[4];
   }
   {
-    // FastDiv::divc assumes positive constant divisors in [2^-100, 2^100]
+    // FastDiv::divc assumes positive constant divisors in [2^-100, 2^100];
+    // the range arguments of divc_q also use k0 and c^2 = gamma k0 / rho0 there
     const double lo = ldexp(1.0, -100), hi = ldexp(1.0, 100);
-    const double cs[5] = {P.rho0, P.cref, P.c2c, P.dx, P.dy};
+    const double cs[7] = {P.rho0, P.cref, P.c2c, P.dx, P.dy, P.k0, P.c2ref};
     for (double v : cs)
       if (!(v >= lo && v <= hi)) {
-        g_err = "rho0, c, c^2, dx, dy must lie in [2^-100, 2^100]";
+        g_err = "rho0, k0, c, c^2, dx, dy must lie in [2^-100, 2^100]";
         return WB_E_ARG;
       }
   }
