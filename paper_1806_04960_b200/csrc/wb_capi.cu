@@ -155,10 +155,10 @@ static dim3 step_grid(const wb_handle* h, int nt) {
 }
 
 // CTA width of each launch variant (WB_KSTEP_VARIANT)
-static const int kVariantNT[10] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64};
+static const int kVariantNT[11] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64, 32};
 static int step_nt(const wb_handle* h, bool debug) {
   if (!h->g1 || debug) return 64;
-  return (h->variant >= 0 && h->variant < 10) ? kVariantNT[h->variant] : 64;
+  return (h->variant >= 0 && h->variant < 11) ? kVariantNT[h->variant] : 64;
 }
 
 // Which column strips of the step grid a launch covers: all of them, only the
@@ -204,6 +204,7 @@ static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
     case 7: WB_LAUNCH((k_step<96, 4, true, false>), 96); break;
     case 8: WB_LAUNCH((k_step_r<64, 200, true>), 64); break;
     case 9: WB_LAUNCH((k_step_r<64, 224, true>), 64); break;
+    case 10: WB_LAUNCH((k_step<32, 8, true, false>), 32); break;
     default: WB_LAUNCH((k_step<64, 1, true, false>), 64);
   }
 #undef WB_LAUNCH
@@ -438,7 +439,7 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
     const long long ctas128 = (long long)((G.nxl + 123) / 124) * ((G.ny + 63) / 64);
     h->variant = ctas128 >= 148 * 4 ? 6 : 0;
   }
-  const int nt = (h->variant >= 0 && h->variant < 10) ? kVariantNT[h->variant] : 64;
+  const int nt = (h->variant >= 0 && h->variant < 11) ? kVariantNT[h->variant] : 64;
   // keep at least ~4 CTAs per SM on small grids: a CTA marches its rows
   // sequentially, so on a small grid the step time is the row latency times
   // the rows per CTA (C1 200x100: 0.093 ms/step at 8 rows, 0.055 at 2)
