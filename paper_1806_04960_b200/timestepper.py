@@ -102,6 +102,9 @@ class Simulation:
             raise SimulationError(f"q0 must have shape {(nx, ny, 5)}, got {q0.shape}")
         self._L = _lib.load()
         self._fluid = np.asarray(grid.mask) != 0
+        # flat indices of the solid cells (usually none): a boolean-mask gather
+        # over the whole grid would cost ~0.1 s per transfer at 4096 x 16384
+        self._solid_flat = np.flatnonzero(~self._fluid.ravel())
         self._n_fluid = int(np.count_nonzero(self._fluid))
         self._ycent = np.ascontiguousarray(grid.y_centers, dtype=np.float64)
         self._yfaces = np.ascontiguousarray(grid.y_faces, dtype=np.float64)
@@ -139,7 +142,7 @@ class Simulation:
         q = np.ascontiguousarray(q, dtype=np.float64)
         # solid cells never change (kernels.py:1241-1244); keep their host
         # values so that sim.q returns them bit-exactly
-        self._solid_q = q[~self._fluid].copy()
+        self._solid_q = q.reshape(-1, 5)[self._solid_flat].copy()
         bi, bj = ctypes.c_int32(-1), ctypes.c_int32(-1)
         rc = self._L.wb_set_state(self._h, q.ctypes.data_as(ctypes.c_void_p), 0,
                                   self.grid.nx, 0, ctypes.byref(bi), ctypes.byref(bj))
@@ -154,8 +157,8 @@ class Simulation:
         q = out if out is not None else np.empty((nx, ny, 5))
         check(self._L.wb_get_state_buf(self._h, q.ctypes.data_as(ctypes.c_void_p), which, 0),
               "wb_get_state")
-        if self._solid_q.size:
-            q[~self._fluid] = self._solid_q
+        if self._solid_flat.size:
+            q.reshape(-1, 5)[self._solid_flat] = self._solid_q
         return q
 
     @property
