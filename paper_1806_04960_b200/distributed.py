@@ -107,7 +107,13 @@ class DeviceSlab:
         _lib.check(self.L.wb_halo_count(h, ctypes.byref(n)), "wb_halo_count")
         self.send = torch.zeros(n.value, dtype=torch.float64, device=f"cuda:{device}")
         self.recv = torch.zeros(n.value, dtype=torch.float64, device=f"cuda:{device}")
-        self.n_fluid = int(np.count_nonzero(np.asarray(grid.mask)[i0:i1]))
+        self._n_fluid = None  # counted on first use (not part of an upload)
+
+    @property
+    def n_fluid(self):
+        if self._n_fluid is None:
+            self._n_fluid = int(np.count_nonzero(np.asarray(self.grid.mask)[self.i0:self.i1]))
+        return self._n_fluid
 
     def stream_ctx(self):
         return self.torch.cuda.stream(self.stream)
