@@ -19,7 +19,8 @@ ref = None
 for v in variants:
     os.environ["WB_KSTEP_VARIANT"] = str(v)
     sim = Simulation(sc.grid, sc.params, sc.q0, sc.boundary)
-    sim.run_steps(3, chunk=3)
+    warm = int(os.environ.get("WB_VB_WARM", "3"))
+    sim.run_steps(warm, chunk=min(warm, 16))
     md, ms, mt = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     _lib.check(sim._L.wb_profile_steps(sim._h, 5, ctypes.byref(md), ctypes.byref(ms),
                                        ctypes.byref(mt)), "profile")
