@@ -286,7 +286,7 @@ class OracleSlab:
 
     def __init__(self, grid, params, q_cols, col0, boundary, cfl, i0, i1):
         import torch
-        from paper_1806_04960_b200.grid import BoundaryCondition, BoundarySpec, build_grid
+        from paper_1806_04960_b200.grid import BoundaryCondition, BoundarySpec
         nx, ny = grid.nx, grid.ny
         self.nx, self.ny, self.i0, self.i1 = nx, ny, i0, i1
         self.lo, self.hi = max(0, i0 - self.HALO), min(nx, i1 + self.HALO)

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import WbConfig, WbError, WbStatus, WbStageArrays, check, dptr, u8ptr
-from .errors import DeviceError, SimulationError, UnsupportedConfigurationError
+from .errors import SimulationError, UnsupportedConfigurationError
 from .grid import BoundarySpec, EdgeSet, KIND_CODES, SIDES
 
 __all__ = ["Simulation", "set_workers", "compute_dt", "advance_step", "total_mass",

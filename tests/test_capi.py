@@ -4,8 +4,6 @@ import ctypes
 import os
 import re
 
-import pytest
-
 from paper_1806_04960_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
