@@ -66,7 +66,10 @@ typedef struct {
 /* Simulation.__init__ (timestepper.py:51-103): grid, params, boundary and
  * per-face BC classification.  mask is the global (nx, ny) uint8 array
  * (grid.py:35); xcent/ycent/yfaces are grid.x_centers/y_centers/y_faces
- * (grid.py:40-54), passed so the device uses the reference's exact doubles. */
+ * (grid.py:40-54), passed so the device uses the reference's exact doubles.
+ * rho0, k0, c = sqrt(gamma k0 / rho0), c^2, dx and dy must lie in
+ * [2^-100, 2^100] (the exact-division scheme's constant range; every
+ * physical configuration does): WB_E_ARG otherwise. */
 int wb_create(const wb_config* cfg, const uint8_t* mask, const double* xcent,
               const double* ycent, const double* yfaces, wb_handle** out);
 int wb_destroy(wb_handle* h);
