@@ -43,7 +43,10 @@ __global__ void k_set_run(Status* st, int mode, int has_max_dt, double max_dt, d
   st->t_end = t_end;
   st->tiny = tiny;
   st->max_steps = max_steps;
-  if (reset_stop) st->stop = 0;
+  // a reached target (stop = -1, set by k_finalize at t_end / max_steps) never
+  // carries over into the next step; error stops (> 0) stay sticky unless the
+  // caller resets them
+  if (reset_stop || st->stop < 0) st->stop = 0;
 }
 __global__ void k_reset_state(Status* st, double t, long long step) {
   st->rmax_bits = 0ull;
@@ -730,6 +733,7 @@ int wb_run(wb_handle* h, double t_end, int64_t max_steps, int32_t chunk, wb_erro
     g_err = "wb_run needs t_end or max_steps";
     return WB_E_ARG;
   }
+  if (mode == 0 && max_steps <= h->step) return WB_OK;  // nothing left to take
   if (h->need_prepare) {
     wb_error e{};
     int rc = do_prepare(h, nullptr, &e);

@@ -319,10 +319,12 @@ class DistributedSimulation:
         """q of global cell (i, j) from its owner, via a SUM all-reduce."""
         import torch
         owner = self.be.i0 <= i < self.be.i1
-        q = self.be.cell_q(i, j) if owner else np.zeros(5)
+        # non-owners contribute -0.0, the exact identity of IEEE addition
+        # (+0.0 would turn a -0.0 component of the owner's cell into +0.0)
+        q = self.be.cell_q(i, j) if owner else np.full(5, -0.0)
         dev = self.be.red.device
-        t = torch.tensor(q, dtype=torch.float64, device=dev if self._nccl else "cpu")
-        with self._ctx():
+        with self._ctx():  # the H2D copy and the collective on the same stream
+            t = torch.tensor(q, dtype=torch.float64, device=dev if self._nccl else "cpu")
             self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
 

@@ -359,7 +359,10 @@ class Simulation:
         return self._t
 
     def run_steps(self, n, chunk=16):
-        """Device-side loop of exactly n steps (no time limit)."""
+        """Device-side loop of exactly n steps (no time limit); n <= 0 takes
+        no step (like DistributedSimulation.run_steps)."""
+        if int(n) <= 0:
+            return self._step
         e = WbError()
         check(self._L.wb_run(self._h, math.nan, self._step + int(n), int(chunk),
                              ctypes.byref(e)), "wb_run")
