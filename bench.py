@@ -87,50 +87,155 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_baseline(seconds=12.0, res=(1024, 2048)):
-    """Reference algorithm (C oracle, all host threads) on a bounded sample of
-    the same workload: wall-impact over the same domain at a reduced grid."""
+def slab():
+    """Per-GPU workload grid; WB_BENCH_SLAB=NXxNY shrinks it (CPU tests only)."""
+    v = os.environ.get("WB_BENCH_SLAB")
+    if v:
+        a, b = v.lower().split("x")
+        return int(a), int(b)
+    return SLAB
+
+
+def bench_config(nx, ny, n_fluid, gpus, extra=None):
+    """The workload description shared by both arms (same dict = same config)."""
+    c = {"workload": f"wall-impact (C5) dambreak, x-slab {nx // gpus}x{ny} per GPU",
+         "grid": [nx, ny], "fluid_cells": n_fluid, "domain": [0, 3.2, 0, 1.8],
+         "l2": "state 4.3 GB per GPU >> 126 MB L2 (no flush needed)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as orc  # CPU-baseline leg only
+    import oracle as orc  # CPU-baseline / reference-arm legs only
+    return orc
+
+
+def oracle_window(res, warmup, steps, threads, budget_s):
+    """The reference algorithm (C restatement in oracle/, pinned bit-exactly to
+    the reference) on the bench workload and the bench's step window: `warmup`
+    untimed steps, then up to `steps` timed steps (stopping early once
+    `budget_s` of wall time is used).  Returns (cell-updates/s, steps timed,
+    seconds)."""
+    orc = _oracle()
     from paper_1806_04960_b200.scenarios import build_scenario
-    cores = os.cpu_count() or 1
-    orc.set_threads(cores)
+    orc.set_threads(threads)
     sc = build_scenario("wall-impact", res)
     sim = orc.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
-    sim.advance()  # warm-up (page-in, thread pool)
+    sim.run_steps(warmup)
     n_fluid = sc.grid.fluid_cell_count()
     t0 = time.perf_counter()
-    steps = 0
-    while time.perf_counter() - t0 < seconds and steps < 200:
+    k = 0
+    while k < steps and (k == 0 or time.perf_counter() - t0 < budget_s):
         sim.advance()
-        steps += 1
+        k += 1
     wall = time.perf_counter() - t0
-    return {"value": n_fluid * steps / wall, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"wall-impact {res[0]}x{res[1]} (same domain), {steps} steps, "
-                      f"{wall:.1f} s, C restatement of the reference (oracle/), "
-                      f"{cores} OpenMP threads"}
+    del sim
+    return n_fluid * k / wall, k, wall
+
+
+def numba_check(res=(1024, 2048), steps=3):
+    """The stock reference (wbflow, Numba, installed unmodified in
+    baseline/_ref) and the port on the same bounded sample, at all host
+    threads and at workers=1: validates the port's speed relative to the
+    reference's own CPU path (timestepper.py:213-217 cells_per_second)."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "wbflow")):
+        return {"unavailable": "baseline/_ref not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "wb_numba_cache"))
+    sys.path.insert(0, ref_dir)
+    try:
+        from wbflow import timestepper as TS
+        from wbflow.grid import BoundaryCondition as RBC, BoundarySpec as RBS
+    except Exception as e:  # numba missing etc.
+        return {"unavailable": f"cannot import the reference: {e}"}
+    from paper_1806_04960_b200.scenarios import build_scenario
+    sc = build_scenario("wall-impact", res)
+    conv = lambda c: RBC(c.kind, c.state, c.segment)  # noqa: E731
+    b = sc.boundary
+    rb = RBS(conv(b.left), conv(b.right), conv(b.bottom), conv(b.top))
+    n_fluid = sc.grid.fluid_cell_count()
+    cores = os.cpu_count() or 1
+    out = {"grid": list(res), "steps": steps, "unit": UNIT}
+    for label, w in (("all_threads", cores), ("workers_1", 1)):
+        t_jit = time.perf_counter()
+        sim = TS.Simulation(sc.grid, sc.params, sc.q0, rb, cfl=0.45, workers=w)
+        sim.advance()  # JIT compile (first call) + warm-up
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            sim.advance()
+        wall = time.perf_counter() - t0
+        out[f"numba_{label}"] = n_fluid * steps / wall
+        if label == "all_threads":
+            out["numba_setup_and_jit_s"] = t0 - t_jit
+        del sim
+        v, k, wall = oracle_window(res, 1, steps, w, 1e9)
+        out[f"port_{label}"] = v
+    out["port_over_numba_all_threads"] = out["port_all_threads"] / out["numba_all_threads"]
+    out["port_over_numba_workers_1"] = out["port_workers_1"] / out["numba_workers_1"]
+    out["cores"] = cores
+    return out
+
+
+def cpu_baseline(args, res, budget_s=20.0):
+    """Reference algorithm on the host cores over a bounded sample of the SAME
+    workload and window as the GPU line (the slab, W warm-up steps, then up to
+    K steps within ~budget_s)."""
+    cores = os.cpu_count() or 1
+    v, k, wall = oracle_window(res, args.warmup, args.steps, cores, budget_s)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"wall-impact {res[0]}x{res[1]} (the bench slab), steps "
+                      f"{args.warmup + 1}-{args.warmup + k} after {args.warmup} untimed "
+                      f"warm-up steps, {wall:.1f} s, C restatement of the reference "
+                      f"(oracle/, bit-identical to it), {cores} OpenMP threads"}
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm on the host CPU on the same
+    workload and step window as our arm (N = 1); rank 0 only under torchrun,
+    where it runs one GPU's slab of the weak-scaling grid."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    samples = []
-    for _ in range(args.warmup):
-        cpu_baseline(seconds=2.0)
-    for _ in range(max(1, min(args.steps, 3))):
-        samples.append(cpu_baseline(seconds=8.0))
-    v = float(np.median([s["value"] for s in samples]))
-    base = samples[-1]
+    nx, ny = slab()
+    from paper_1806_04960_b200.grid import build_grid  # noqa: F401  (package import check)
+    from paper_1806_04960_b200.scenarios import build_scenario
+    n_fluid = build_scenario("wall-impact", (nx, ny)).grid.fluid_cell_count()
+    cores = os.cpu_count() or 1
+    v, k, wall = oracle_window((nx, ny), args.warmup, args.steps, cores, 240.0)
+    base = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"wall-impact {nx}x{ny}: steps {args.warmup + 1}-{args.warmup + k} "
+                      f"after {args.warmup} untimed warm-up steps ({wall:.1f} s), C "
+                      f"restatement of the reference (oracle/, bit-identical to it), "
+                      f"{cores} OpenMP threads"}
+    if os.environ.get("WB_BENCH_NUMBA", "1") != "0":
+        base["numba_check"] = numba_check()
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "steps": k, "warmup": args.warmup, "ms_per_step": wall / k * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": v / PUBLISHED,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "wall-impact (C5) dambreak, bounded CPU sample",
-                       "grid": [1024, 2048]},
-            "cpu_baseline": {**base, "value": v},
+            "config": bench_config(nx, ny, n_fluid, 1),
+            "cpu_baseline": base,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if args.gpus > 1:
+        line["config"]["note"] = ("one GPU's slab of the weak-scaling grid: the full "
+                                  f"{nx * args.gpus}x{ny} grid needs "
+                                  f"{nx * args.gpus * ny * 560 / 2**30:.0f} GiB of host memory")
     print(json.dumps(line), flush=True)
 
 
@@ -148,7 +253,7 @@ def run_ours(args):
         args.gpus = 1
     dev = 0
     torch.cuda.set_device(dev)
-    nx, ny = SLAB
+    nx, ny = slab()
     sc = build_scenario("wall-impact", (nx, ny))
     n_fluid = sc.grid.fluid_cell_count()
     sim = Simulation(sc.grid, sc.params, sc.q0, sc.boundary, device=dev)
@@ -226,24 +331,44 @@ def run_ours(args):
     sim.q = q_host                      # H2D of the state
     for _ in range(args.steps):
         sim.advance()                   # per step: dt + status read back
-    sim._get_q(0, out=out_host)         # D2H of the result
+    sim.get_state(out=out_host)         # D2H of the result
     e2e_wall = time.perf_counter() - t0
     state_bytes = nx * ny * 5 * 8
     e2e = {"value": n_fluid * args.steps / e2e_wall, "unit": UNIT,
            "h2d_bytes_per_step": state_bytes / args.steps,
            "d2h_bytes_per_step": state_bytes / args.steps + 32 + 96,
            "api": "Simulation(q0 host) -> advance() x K -> sim.q (host)"}
-    base = cpu_baseline() if not args.no_cpu else None
+    # ---- developed flow: the same K steps from a state 300 steps further on
+    # (more solved x-faces, gas "dust" exercising the exact-replay path);
+    # the state is advanced outside the timed region ----
+    dev_line = None
+    if not args.no_developed:
+        sim.q = q_host                  # back to q0 (pinned host copy), t = 0
+        sim.t, sim.step_count = 0.0, 0
+        sim.run_steps(300, chunk=20)
+        torch.cuda.synchronize()
+        c0 = sim.work_counters()["replays"]
+        e0.record(stream)
+        sim.run_steps(args.steps, chunk=max(d for d in range(1, 17) if args.steps % d == 0))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1)
+        wcd = sim.work_counters()
+        dev_line = {"start_step": sim.step_count - args.steps, "steps": args.steps,
+                    "ms_per_step": dms / args.steps,
+                    "value": n_fluid * args.steps / (dms * 1e-3), "unit": UNIT,
+                    "counters_last_step": {k: wcd[k] for k in ("n_second_order", "x_faces",
+                                                               "y_faces")},
+                    "exact_replays": wcd["replays"] - c0}
+    base = cpu_baseline(args, (nx, ny)) if not args.no_cpu else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PUBLISHED,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "wall-impact (C5) dambreak, x-slab 4096x16384 per GPU",
-                       "grid": [nx, ny], "fluid_cells": n_fluid, "domain": [0, 3.2, 0, 1.8],
-                       "l2": "state 4.3 GB per GPU >> 126 MB L2 (no flush needed)",
-                       "parallelism": f"x-slab dp{args.gpus}"},
+            "config": bench_config(nx, ny, n_fluid, 1),
+            "parallelism": f"x-slab dp{args.gpus}",
             "roofline": roof, "cpu_baseline": base, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk}
+            "developed": dev_line, "clocks": clk}
     print(json.dumps(line), flush=True)
 
 
@@ -272,7 +397,7 @@ def run_ours_distributed(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     else:
         dist.init_process_group(backend)
-    nx, ny = SLAB[0] * world, SLAB[1]
+    nx, ny = slab()[0] * world, slab()[1]
     i0, i1 = slab_bounds(nx, world, rank)
     lo, hi = stored_range(nx, i0, i1)
     sc = build_scenario("wall-impact", (nx, ny), columns=(lo, hi))
@@ -339,11 +464,9 @@ def run_ours_distributed(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PUBLISHED,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "wall-impact (C5) dambreak, x-slab 4096x16384 per GPU",
-                           "grid": [nx, ny], "fluid_cells": n_fluid,
-                           "parallelism": f"x-slab dp{world}, {backend} halo send/recv + one "
-                                          "MAX all-reduce per step",
-                           "l2": "state 4.3 GB per GPU >> 126 MB L2 (no flush needed)"},
+                "config": bench_config(nx, ny, n_fluid, world),
+                "parallelism": f"x-slab dp{world}, {backend} halo send/recv + one "
+                               "MAX all-reduce per step",
                 # per step: set_run, reset_counters, k_step, prefinalize, finalize,
                 # pack_halo, unpack_halo
                 "gpu_launches": 7 * args.steps,
@@ -370,6 +493,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-developed", action="store_true",
+                    help="skip the developed-flow window (steps 300-K..300)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -61,6 +61,7 @@ typedef struct {
   int32_t stop;              /* 0 running, >0 error code, -1 target reached */
   int32_t cur;
   uint64_t n_second_order, x_faces_solved, y_faces_solved; /* last step */
+  uint64_t replays;          /* exact IEEE unit replays since wb_create (cumulative) */
 } wb_status;
 
 /* Simulation.__init__ (timestepper.py:51-103): grid, params, boundary and

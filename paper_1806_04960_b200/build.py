@@ -8,6 +8,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "wb_capi.cu")
 LIB = os.path.join(HERE, "libwbflow_b200.so")
+# test build of the same sources with every speculative FastDiv unit rejected
+# (-DWB_FORCE_REPLAY): all cells, faces and updates take the exact IEEE replay
+# path, which tests/test_gpu_replay.py runs against the oracle
+LIB_REPLAY = os.path.join(HERE, "libwbflow_b200_replay.so")
 
 # --fmad=false: the reference never contracts a*b+c (Numba/LLVM without
 # fastmath); IEEE division/sqrt are nvcc's double-precision defaults and
@@ -23,24 +27,31 @@ def sources():
         [os.path.join(ROOT, "include", "wbflow_b200.h")]
 
 
-def needs_build():
-    if not os.path.exists(LIB):
+def needs_build(lib=LIB):
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
-        return LIB
+def build(force=False, verbose=False, replay=True):
+    """Compile the product library and (replay=True) the forced-replay test
+    library, both with nvcc for sm_100a, concurrently."""
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, SRC]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libwbflow_b200.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+    jobs = []
+    for lib, extra in ((LIB, []), (LIB_REPLAY, ["-DWB_FORCE_REPLAY"]) if replay else (None, None)):
+        if lib is None or (not force and not needs_build(lib)):
+            continue
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", lib, SRC]
+        jobs.append((lib, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                           stderr=subprocess.PIPE, text=True)))
+    for lib, p in jobs:
+        out, err = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"nvcc failed building {os.path.basename(lib)}")
+        if verbose and lib == LIB:
+            sys.stderr.write(err)
     return LIB
 
 

@@ -159,6 +159,14 @@ static dim3 step_grid(const wb_handle* h, int nt) {
 
 // CTA width of each launch variant (WB_KSTEP_VARIANT)
 static const int kVariantNT[11] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64, 32};
+// variants compiled into this build (the others need -DWB_EXPERIMENTS)
+static bool variant_built(int v) {
+#ifdef WB_EXPERIMENTS
+  return v >= 0 && v < 11;
+#else
+  return v == 0 || v == 3 || v == 5 || v == 6 || v == 7;
+#endif
+}
 static int step_nt(const wb_handle* h, bool debug) {
   if (!h->g1 || debug) return 64;
   return (h->variant >= 0 && h->variant < 11) ? kVariantNT[h->variant] : 64;
@@ -198,16 +206,18 @@ static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
     return;
   }
   switch (h->variant) {
-    case 1: WB_LAUNCH((k_step<64, 6, true, false>), 64); break;
-    case 2: WB_LAUNCH((k_step<64, 8, true, false>), 64); break;
     case 3: WB_LAUNCH((k_step<128, 3, true, false>), 128); break;
-    case 4: WB_LAUNCH((k_step<128, 4, true, false>), 128); break;
     case 5: WB_LAUNCH((k_step<32, 12, true, false>), 32); break;
     case 6: WB_LAUNCH((k_step<128, 2, true, false>), 128); break;
     case 7: WB_LAUNCH((k_step<96, 4, true, false>), 96); break;
+#ifdef WB_EXPERIMENTS
+    case 1: WB_LAUNCH((k_step<64, 6, true, false>), 64); break;
+    case 2: WB_LAUNCH((k_step<64, 8, true, false>), 64); break;
+    case 4: WB_LAUNCH((k_step<128, 4, true, false>), 128); break;
     case 8: WB_LAUNCH((k_step_r<64, 200, true>), 64); break;
     case 9: WB_LAUNCH((k_step_r<64, 224, true>), 64); break;
     case 10: WB_LAUNCH((k_step<32, 8, true, false>), 32); break;
+#endif
     default: WB_LAUNCH((k_step<64, 1, true, false>), 64);
   }
 #undef WB_LAUNCH
@@ -413,6 +423,7 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
     CK(e);
   }
   CK(cudaMalloc(&h->st, sizeof(Status)));
+  CK(cudaMemsetAsync(h->st, 0, sizeof(Status), h->stream));  // counters, tickets, launch id
   CK(cudaHostAlloc(&h->h_st, sizeof(Status), cudaHostAllocDefault));
   CK(cudaMalloc(&h->dtlog, DTLOG_CAP * sizeof(double)));
   CK(cudaMalloc(&h->scratch, 4 * sizeof(unsigned long long)));
@@ -435,6 +446,10 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
   int L = cfg->rows_per_block > 0 ? cfg->rows_per_block : 64;
   if (const char* v = getenv("WB_KSTEP_VARIANT")) {
     h->variant = atoi(v);
+    if (!variant_built(h->variant)) {
+      g_err = "WB_KSTEP_VARIANT names a launch variant that is not built";
+      return WB_E_ARG;
+    }
   } else {
     // 128-thread CTAs (124 owned columns) halve the redundant halo columns of
     // the 64-thread ones (9.69 vs 9.89 ms on the C5 slab) once the grid is
@@ -828,6 +843,7 @@ int wb_get_status(wb_handle* h, wb_status* s) {
   s->n_second_order = d.n2nd;
   s->x_faces_solved = d.nxs;
   s->y_faces_solved = d.nys;
+  s->replays = d.n_replay;
   return WB_OK;
 }
 

@@ -32,6 +32,7 @@ struct Status {
   unsigned long long rmax_used_bits;  // rate the last committed step used for dt
   unsigned long long launch_id;       // incremented before every step launch
   unsigned int ticket[2];  // dynamic CTA index of the step kernel, per concurrent launch
+  unsigned long long n_replay;  // exact IEEE replays of units (cumulative, never reset)
 };
 
 struct Geo {

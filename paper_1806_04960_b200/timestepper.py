@@ -9,7 +9,11 @@ attributes, the module functions ``set_workers`` / ``compute_dt`` /
 ``SimulationError`` messages, step and cell; a failed step is not committed).
 
 The state lives on the GPU in SoA planes; ``sim.q`` is downloaded lazily in
-the reference layout (nx, ny, 5).  The reference's per-step work arrays
+the reference layout (nx, ny, 5) into a cached host mirror.  As in the
+reference, where ``q`` is the live state array (timestepper.py:68, 209),
+in-place writes such as ``sim.q[i, j, 0] *= 1.001`` take effect: a mirror
+handed out by ``sim.q`` is uploaded again before the next device operation
+(step, rate, detection, diagnostics).  ``sim.q_next`` is a read-only copy.  The reference's per-step work arrays
 (fW..fN, vol, psi, quiet, DW..DN, rhoE_c, rhoE_fy) are produced only when the
 simulation is created with ``debug=True`` -- the fused kernel then also
 stores them -- because the production path never materialises them.
@@ -120,6 +124,8 @@ class Simulation:
         self._t = 0.0
         self._step = 0
         self._edges = None
+        self._qh = None           # cached host mirror of the current state
+        self._qh_exposed = False  # handed out by the q property (may be written)
         self._set_q(q0)
         if self.debug:
             for name in ("fW", "fE", "fS", "fN", "vol", "psi", "DW", "DE", "DS", "DN"):
@@ -139,6 +145,8 @@ class Simulation:
 
     # ---- state transfer ---------------------------------------------------
     def _set_q(self, q):
+        self._qh = None
+        self._qh_exposed = False
         q = np.ascontiguousarray(q, dtype=np.float64)
         # solid cells never change (kernels.py:1241-1244); keep their host
         # values so that sim.q returns them bit-exactly
@@ -161,9 +169,27 @@ class Simulation:
             q.reshape(-1, 5)[self._solid_flat] = self._solid_q
         return q
 
+    def _host_q(self):
+        """The current state on the host (cached until the next step)."""
+        if self._qh is None:
+            self._qh = self._get_q(0)
+        return self._qh
+
+    def _flush_q(self):
+        """Upload a mirror the caller may have written through ``sim.q``
+        (reference semantics: q is the live array)."""
+        if self._qh is not None and self._qh_exposed:
+            self._set_q(self._qh)
+
+    def _stepped(self):
+        self._qh = None
+        self._qh_exposed = False
+
     @property
     def q(self):
-        return self._get_q(0)
+        q = self._host_q()
+        self._qh_exposed = True
+        return q
 
     @q.setter
     def q(self, value):
@@ -172,9 +198,18 @@ class Simulation:
             raise SimulationError(f"q must have shape {(self.grid.nx, self.grid.ny, 5)}")
         self._set_q(value)
 
+    def get_state(self, out=None):
+        """Download the current state into ``out`` (an (nx, ny, 5) float64
+        array, e.g. pinned host memory) or a new array; unlike ``sim.q`` it
+        neither caches nor re-uploads."""
+        self._flush_q()
+        return self._get_q(0, out=out)
+
     @property
     def q_next(self):
-        return self._get_q(1)
+        q = self._get_q(1)
+        q.flags.writeable = False  # a copy: writes could not reach the device
+        return q
 
     @property
     def t(self):
@@ -215,6 +250,7 @@ class Simulation:
 
     def detect(self):
         """Column detection of the current state (timestepper.py:132-135)."""
+        self._flush_q()
         r = ctypes.c_double()
         e = WbError()
         check(self._L.wb_max_rate(self._h, ctypes.byref(r), ctypes.byref(e)), "wb_max_rate")
@@ -222,7 +258,7 @@ class Simulation:
 
     def primitive_fields(self):
         """(rho, u, v, alpha, p); solid cells hold zeros (timestepper.py:107-125)."""
-        q = self.q
+        q = self._host_q()
         fluid = self._fluid
         rho = np.zeros_like(q[:, :, 0])
         u = np.zeros_like(rho)
@@ -247,13 +283,14 @@ class Simulation:
         (no download; equal to ~1e-15 relative, different summation order)."""
         if device:
             return self.diagnostics()["mass"]
-        return float(np.sum(self.q[:, :, 0][self._fluid]) * self.grid.cell_area)
+        return float(np.sum(self._host_q()[:, :, 0][self._fluid]) * self.grid.cell_area)
 
     def diagnostics(self, y0_eq=None):
         """Device-side reductions of the current state: mass, max |u|, max |v|,
         alpha range and -- given the surface level ``y0_eq`` of the exact
         water-at-rest profile -- the paper's equilibrium errors E_rho, E_u, E_v,
         E_P (PAPER.md:866-886)."""
+        self._flush_q()
         out = np.empty(9)
         check(self._L.wb_diagnostics(self._h, math.nan if y0_eq is None else float(y0_eq),
                                      dptr(out)), "wb_diagnostics")
@@ -268,6 +305,7 @@ class Simulation:
     def depth_averaged_velocity(self):
         """u_bar(x) per column on the device (see analysis.depth_averaged_velocity
         for the host formula; same terms, j-ordered sums)."""
+        self._flush_q()
         out = np.empty(self.grid.nx)
         check(self._L.wb_depth_averaged_velocity(self._h, dptr(out)),
               "wb_depth_averaged_velocity")
@@ -292,6 +330,7 @@ class Simulation:
 
     def max_rate(self):
         """Detection + CFL rate max of the current state (timestepper.py:143-159)."""
+        self._flush_q()
         r = ctypes.c_double()
         e = WbError()
         check(self._L.wb_max_rate(self._h, ctypes.byref(r), ctypes.byref(e)), "wb_max_rate")
@@ -303,6 +342,7 @@ class Simulation:
     def advance(self, max_dt=None):
         """One step; returns the dt taken (timestepper.py:163-218)."""
         wall0 = time.perf_counter()
+        self._flush_q()
         dt = ctypes.c_double()
         e = WbError()
         mdt = math.nan if max_dt is None else float(max_dt)
@@ -319,6 +359,7 @@ class Simulation:
                   "wb_advance")
         if e.code:
             self._raise(e)
+        self._stepped()
         s = self._sync_time()
         wall = time.perf_counter() - wall0
         self.stats.dt = dt.value
@@ -343,9 +384,11 @@ class Simulation:
             return self._t
         wall0 = time.perf_counter()
         step0 = self._step
+        self._flush_q()
         e = WbError()
         check(self._L.wb_run(self._h, float(t_end), -1 if max_steps is None else int(max_steps),
                              16, ctypes.byref(e)), "wb_run")
+        self._stepped()
         if e.code:
             self._sync_time()
             self._raise(e)
@@ -363,9 +406,11 @@ class Simulation:
         no step (like DistributedSimulation.run_steps)."""
         if int(n) <= 0:
             return self._step
+        self._flush_q()
         e = WbError()
         check(self._L.wb_run(self._h, math.nan, self._step + int(n), int(chunk),
                              ctypes.byref(e)), "wb_run")
+        self._stepped()
         if e.code:
             self._sync_time()
             self._raise(e)
@@ -403,7 +448,8 @@ class Simulation:
     def work_counters(self):
         s = self._sync_time()
         return {"n_second_order": int(s.n_second_order), "x_faces": int(s.x_faces_solved),
-                "y_faces": int(s.y_faces_solved), "n_fluid": self._n_fluid}
+                "y_faces": int(s.y_faces_solved), "n_fluid": self._n_fluid,
+                "replays": int(s.replays)}
 
 
 def compute_dt(sim, cfl=None):

@@ -28,11 +28,17 @@ def case_names():
 
 
 def same(a, b):
-    """Bit-level equality (NaN positions included, +0 == -0 as IEEE)."""
+    """Bit-level equality: every double has the same bit pattern (so +0 and -0
+    differ); NaNs match NaNs of any payload."""
     a = np.asarray(a)
     b = np.asarray(b)
     if a.shape != b.shape:
         return False
     if a.dtype.kind == "f":
-        return bool(np.array_equal(a, b, equal_nan=True))
+        a64 = np.ascontiguousarray(a, dtype=np.float64)
+        b64 = np.ascontiguousarray(b, dtype=np.float64)
+        eq = a64.view(np.int64) == b64.view(np.int64)
+        if not eq.all():
+            eq |= np.isnan(a64) & np.isnan(b64)
+        return bool(eq.all())
     return bool(np.array_equal(a, b))

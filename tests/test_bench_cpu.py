@@ -10,8 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
-                         timeout=300, cwd=ROOT)
+                          "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT,
+                         env=dict(os.environ, WB_BENCH_SLAB="128x256", WB_BENCH_NUMBA="0"))
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
     assert len(lines) == 1
@@ -23,3 +24,4 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["grid"] == [128, 256] and d["steps"] == 2
