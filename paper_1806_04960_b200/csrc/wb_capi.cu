@@ -5,6 +5,8 @@
 // captures multi-step chunks in a CUDA graph for device-side run loops, and
 // translates device status into the reference's error contract.  No torch
 // types cross this boundary.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -33,6 +35,7 @@ static thread_local std::string g_err;
 namespace {
 constexpr int NT = 64;
 constexpr long long DTLOG_CAP = 1 << 20;
+constexpr size_t PLANE_SHIFT = 2;  // doubles; see wb_create
 
 // small kernel that sets the run parameters in the device status
 __global__ void k_set_run(Status* st, int mode, int has_max_dt, double max_dt, double t_end,
@@ -89,6 +92,9 @@ struct wb_handle {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* planes = nullptr;
   uint8_t* mask = nullptr;
+  // TMA descriptors of the plane stack and the mask, one pair per CTA width
+  // (box {NT, 1, 4} / {NT, 1}); index NT / 32 - 1
+  CUtensorMap tq[4], tm[4];
   double *y0s = nullptr, *aeqs = nullptr, *ycent = nullptr, *yfaces = nullptr,
          *xcent = nullptr;
   double *ch_sum = nullptr, *ch_aeq = nullptr;
@@ -157,6 +163,87 @@ static dim3 step_grid(const wb_handle* h, int nt) {
   return dim3((h->G.nxl + nt - 2 * HALO - 1) / (nt - 2 * HALO), (h->G.ny + h->L - 1) / h->L);
 }
 
+// TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry
+// point, so the library needs no -lcuda).  q: 3-D {pitch, ny, 8 planes}
+// FP64 with box {nt, 1, 4} (plane coordinate cur*4 selects the buffer);
+// mask: 2-D {pitch, ny} u8 with box {nt, 1}.  Out-of-range rows / columns
+// are zero-filled.
+static int make_tensor_maps(wb_handle* h) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+    if (qr != cudaDriverEntryPointSuccess || !fn) {
+      g_err = "cuTensorMapEncodeTiled not available";
+      return WB_E_CUDA;
+    }
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const Geo& G = h->G;
+  const size_t plane = (size_t)G.pitch * G.ny;
+  for (int k = 0; k < 4; k++) {
+    const cuuint32_t nt = 32u * (k + 1);
+    cuuint64_t qdim[3] = {(cuuint64_t)G.pitch, (cuuint64_t)G.ny, 8};
+    cuuint64_t qstr[2] = {(cuuint64_t)G.pitch * sizeof(double), plane * sizeof(double)};
+    cuuint32_t qbox[3] = {nt, 1, 4};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode(&h->tq[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, h->B.q[0][0], qdim, qstr,
+                        qbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      g_err = "cuTensorMapEncodeTiled (state planes) failed";
+      return WB_E_CUDA;
+    }
+    cuuint64_t mdim[2] = {(cuuint64_t)G.pitch, (cuuint64_t)G.ny};
+    cuuint64_t mstr[1] = {(cuuint64_t)G.pitch};
+    cuuint32_t mbox[2] = {nt, 1};
+    r = encode(&h->tm[k], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, h->mask, mdim, mstr, mbox, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      g_err = "cuTensorMapEncodeTiled (mask) failed";
+      return WB_E_CUDA;
+    }
+  }
+  return WB_OK;
+}
+
+// dynamic shared memory of every built k_step instantiation (> 48 KB needs
+// the opt-in attribute)
+template <int NTV, int MB, bool G1, bool DBG>
+static cudaError_t step_attr() {
+  cudaError_t e = cudaFuncSetAttribute(k_step<NTV, MB, G1, DBG>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       step_smem_bytes<NTV>());
+  if (e != cudaSuccess) return e;
+  // the shared-memory rings are the point: prefer the largest carveout
+  return cudaFuncSetAttribute(k_step<NTV, MB, G1, DBG>,
+                              cudaFuncAttributePreferredSharedMemoryCarveout,
+                              (int)cudaSharedmemCarveoutMaxShared);
+}
+static int init_step_kernels() {
+  CK((step_attr<64, 1, true, false>()));
+  CK((step_attr<64, 1, true, true>()));
+  CK((step_attr<64, 1, false, false>()));
+  CK((step_attr<64, 1, false, true>()));
+  CK((step_attr<128, 2, true, false>()));
+  CK((step_attr<128, 3, true, false>()));
+  CK((step_attr<96, 4, true, false>()));
+  CK((step_attr<32, 12, true, false>()));
+#ifdef WB_EXPERIMENTS
+  CK((step_attr<64, 6, true, false>()));
+  CK((step_attr<64, 8, true, false>()));
+  CK((step_attr<128, 4, true, false>()));
+  CK((step_attr<32, 8, true, false>()));
+  CK(cudaFuncSetAttribute(k_step_r<64, 200, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          step_smem_bytes<64>()));
+  CK(cudaFuncSetAttribute(k_step_r<64, 224, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          step_smem_bytes<64>()));
+#endif
+  return WB_OK;
+}
+
 // CTA width of each launch variant (WB_KSTEP_VARIANT)
 static const int kVariantNT[11] = {64, 64, 64, 128, 128, 32, 128, 96, 64, 64, 32};
 // variants compiled into this build (the others need -DWB_EXPERIMENTS)
@@ -196,7 +283,9 @@ static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
     part = Part{1, 1, 0};
     g.x -= 2;
   }
-#define WB_LAUNCH(K, NTV) K<<<g, NTV, 0, s>>>(G, h->B, h->P, h->L, D, part)
+#define WB_LAUNCH(K, NTV)                                                          \
+  K<<<g, NTV, step_smem_bytes<NTV>(), s>>>(G, h->B, h->P, h->L, D, part, h->tq[NTV / 32 - 1], \
+                                          h->tm[NTV / 32 - 1])
   if (!h->g1) {
     WB_LAUNCH((k_step<64, 1, false, DEBUG>), 64);
     return;
@@ -386,10 +475,13 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
   }
 
   const size_t plane = (size_t)G.pitch * G.ny;
-  CK(cudaMalloc(&h->planes, 8 * plane * sizeof(double)));
-  CK(cudaMemsetAsync(h->planes, 0, 8 * plane * sizeof(double), h->stream));
+  // PLANE_SHIFT doubles in front of the stack: stored column HALO (the first
+  // owned one) then starts a 32-B sector, so every CTA strip's owned columns
+  // (a multiple of 4 doubles wide) write whole sectors
+  CK(cudaMalloc(&h->planes, (8 * plane + 2 * PLANE_SHIFT) * sizeof(double)));
+  CK(cudaMemsetAsync(h->planes, 0, (8 * plane + 2 * PLANE_SHIFT) * sizeof(double), h->stream));
   for (int b = 0; b < 2; b++)
-    for (int m = 0; m < 4; m++) h->B.q[b][m] = h->planes + (b * 4 + m) * plane;
+    for (int m = 0; m < 4; m++) h->B.q[b][m] = h->planes + PLANE_SHIFT + (b * 4 + m) * plane;
   // mask in device layout (j, stored column), zero outside the domain
   {
     uint8_t* hm = (uint8_t*)calloc(plane, 1);
@@ -432,6 +524,12 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
 
   Bufs& B = h->B;
   B.mask = h->mask;
+  {
+    int rc = make_tensor_maps(h);
+    if (rc) return rc;
+    rc = init_step_kernels();
+    if (rc) return rc;
+  }
   B.y0s[0] = h->y0s;
   B.y0s[1] = h->y0s + G.pitch;
   B.aeqs[0] = h->aeqs;
@@ -452,10 +550,11 @@ static int create_body(wb_handle* h, const wb_config* cfg, const uint8_t* mask,
     }
   } else {
     // 128-thread CTAs (124 owned columns) halve the redundant halo columns of
-    // the 64-thread ones (9.69 vs 9.89 ms on the C5 slab) once the grid is
-    // large enough to keep 4 such CTAs per SM busy at 64 rows per CTA
+    // the 64-thread ones once the grid is large enough to keep several such
+    // CTAs per SM busy at 64 rows per CTA; with the row state in shared
+    // memory (162 registers) three of them fit per SM (12 warps)
     const long long ctas128 = (long long)((G.nxl + 123) / 124) * ((G.ny + 63) / 64);
-    h->variant = ctas128 >= 148 * 4 ? 6 : 0;
+    h->variant = ctas128 >= 148 * 4 ? 3 : 0;
   }
   const int nt = (h->variant >= 0 && h->variant < 11) ? kVariantNT[h->variant] : 64;
   // keep at least ~4 CTAs per SM on small grids: a CTA marches its rows

@@ -48,6 +48,11 @@ def test_forced_replay_build_is_bitexact(cuda):
     r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=1500)
     sys.stdout.write(r.stdout[-3000:])
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    # 12 golden cases + 5 stage-array cases + error path + 2 run_until + initial
+    # state + the replay-counter check, none skipped
+    import re
+    m = re.search(r"(\d+) passed", r.stdout)
+    assert m and int(m.group(1)) >= 22 and "skipped" not in r.stdout.split("\n")[-2], r.stdout[-2000:]
 
 
 def test_child_replay_counter(cuda):
