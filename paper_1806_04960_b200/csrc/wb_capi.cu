@@ -166,7 +166,7 @@ static dim3 step_grid(const wb_handle* h, int nt) {
 // TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry
 // point, so the library needs no -lcuda).  q: 3-D {pitch, ny, 8 planes}
 // FP64 with box {nt, 1, 4} (plane coordinate cur*4 selects the buffer);
-// mask: 2-D {pitch, ny} u8 with box {nt, 1}.  Out-of-range rows / columns
+// mask: 2-D {pitch, ny} u8 with box {nt + 16, 1}.  Out-of-range rows / columns
 // are zero-filled.
 static int make_tensor_maps(wb_handle* h) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -197,7 +197,7 @@ static int make_tensor_maps(wb_handle* h) {
     }
     cuuint64_t mdim[2] = {(cuuint64_t)G.pitch, (cuuint64_t)G.ny};
     cuuint64_t mstr[1] = {(cuuint64_t)G.pitch};
-    cuuint32_t mbox[2] = {nt, 1};
+    cuuint32_t mbox[2] = {nt + 16, 1};  // starts at a 16-column boundary (see k_step)
     r = encode(&h->tm[k], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, h->mask, mdim, mstr, mbox, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
