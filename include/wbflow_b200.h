@@ -62,6 +62,8 @@ typedef struct {
   int32_t cur;
   uint64_t n_second_order, x_faces_solved, y_faces_solved; /* last step */
   uint64_t replays;          /* exact IEEE unit replays since wb_create (cumulative) */
+  uint64_t replays_by_kind[6]; /* reconstruction, flux_y(S), x-face, flux_x pair, y-face,
+                                  update */
 } wb_status;
 
 /* Simulation.__init__ (timestepper.py:51-103): grid, params, boundary and

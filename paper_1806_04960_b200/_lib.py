@@ -45,7 +45,8 @@ class WbStatus(ctypes.Structure):
     _fields_ = [("t", ctypes.c_double), ("dt", ctypes.c_double), ("rmax", ctypes.c_double),
                 ("step", ctypes.c_int64), ("stop", ctypes.c_int32), ("cur", ctypes.c_int32),
                 ("n_second_order", ctypes.c_uint64), ("x_faces_solved", ctypes.c_uint64),
-                ("y_faces_solved", ctypes.c_uint64), ("replays", ctypes.c_uint64)]
+                ("y_faces_solved", ctypes.c_uint64), ("replays", ctypes.c_uint64),
+                ("replays_by_kind", ctypes.c_uint64 * 6)]
 
 
 class WbStageArrays(ctypes.Structure):

@@ -943,6 +943,7 @@ int wb_get_status(wb_handle* h, wb_status* s) {
   s->x_faces_solved = d.nxs;
   s->y_faces_solved = d.nys;
   s->replays = d.n_replay;
+  for (int k = 0; k < 6; k++) s->replays_by_kind[k] = d.n_replay_kind[k];
   return WB_OK;
 }
 

@@ -33,6 +33,7 @@ struct Status {
   unsigned long long launch_id;       // incremented before every step launch
   unsigned int ticket[2];  // dynamic CTA index of the step kernel, per concurrent launch
   unsigned long long n_replay;  // exact IEEE replays of units (cumulative, never reset)
+  unsigned long long n_replay_kind[6];  // the same per unit kind (see WB_REPLAY)
 };
 
 struct Geo {

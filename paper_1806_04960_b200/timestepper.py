@@ -449,7 +449,10 @@ class Simulation:
         s = self._sync_time()
         return {"n_second_order": int(s.n_second_order), "x_faces": int(s.x_faces_solved),
                 "y_faces": int(s.y_faces_solved), "n_fluid": self._n_fluid,
-                "replays": int(s.replays)}
+                "replays": int(s.replays),
+                "replays_by_kind": dict(zip(("reconstruct", "flux_y_S", "x_face", "flux_x_pair",
+                                             "y_face", "update"),
+                                            (int(v) for v in s.replays_by_kind)))}
 
 
 def compute_dt(sim, cfl=None):
