@@ -9,8 +9,8 @@ ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "wb_capi.cu")
 LIB = os.path.join(HERE, "libwbflow_b200.so")
 # test build of the same sources with every speculative FastDiv unit rejected
-# (-DWB_FORCE_REPLAY): all cells, faces and updates take the exact IEEE replay
-# path, which tests/test_gpu_replay.py runs against the oracle
+# (-DWB_FORCE_REPLAY): all cells, faces and updates take the exact IEEE
+# replay path, which tests/test_gpu_replay.py runs against the oracle
 LIB_REPLAY = os.path.join(HERE, "libwbflow_b200_replay.so")
 
 # --fmad=false: the reference never contracts a*b+c (Numba/LLVM without
@@ -39,8 +39,11 @@ def build(force=False, verbose=False, replay=True):
     library, both with nvcc for sm_100a, concurrently."""
     nvcc = os.environ.get("NVCC", "nvcc")
     jobs = []
-    for lib, extra in ((LIB, []), (LIB_REPLAY, ["-DWB_FORCE_REPLAY"]) if replay else (None, None)):
-        if lib is None or (not force and not needs_build(lib)):
+    builds = [(LIB, [])]
+    if replay:
+        builds.append((LIB_REPLAY, ["-DWB_FORCE_REPLAY"]))
+    for lib, extra in builds:
+        if not force and not needs_build(lib):
             continue
         cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", lib, SRC]
         jobs.append((lib, subprocess.Popen(cmd, stdout=subprocess.PIPE,

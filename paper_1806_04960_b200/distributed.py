@@ -202,7 +202,7 @@ class DistributedSimulation:
     torch.distributed process group (the reference's Simulation semantics:
     same dt sequence, same error step/cell, bit-identical state)."""
 
-    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=False):
+    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=False, graphs=True):
         import torch.distributed as dist
         self.dist = dist
         self.be = backend
@@ -222,6 +222,11 @@ class DistributedSimulation:
         # detection chain runs its 256 row segments back to back -- against
         # ~0.05 ms of exchange it could hide.
         self.overlap = overlap and hasattr(backend, "step_begin")
+        # device loops over NCCL are captured once per chunk length as a CUDA
+        # graph (kernels + collectives), replayed without host enqueue work;
+        # set to False after a failed capture (then steps are enqueued eagerly)
+        self.use_graphs = graphs and self._nccl and hasattr(backend, "stream")
+        self._graphs = {}
 
     # -- collectives ------------------------------------------------------
     def _allreduce_max(self, t):
@@ -310,6 +315,39 @@ class DistributedSimulation:
             be.finalize()
             self._halo_exchange()
 
+    def enqueue_steps(self, n):
+        """Enqueue n steps (mode 0: no time limit) without a host sync: as
+        replays of a captured CUDA graph of the step sequence (step kernels,
+        MAX all-reduce, finalize, halo send/recv) when the group is NCCL, else
+        eagerly."""
+        if not self._prepared:
+            self.prepare()
+        if not self.use_graphs:
+            for _ in range(n):
+                self._enqueue_step()
+            return
+        torch = self.be.torch
+        g = self._graphs.get(n)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(g, stream=self.be.stream):
+                    for _ in range(n):
+                        self._enqueue_step()
+            except Exception as e:  # capture unsupported here: eager from now on
+                import warnings
+                warnings.warn(f"CUDA graph capture of the distributed step failed ({e}); "
+                              "enqueueing steps eagerly")
+                self.use_graphs = False
+                torch.cuda.synchronize()
+                for _ in range(n):
+                    self._enqueue_step()
+                return
+            self._graphs[n] = g
+        with self._ctx():  # a graph replays on the current stream: the backend's
+            g.replay()
+
     def _sync(self):
         s = self.be.status()
         self.t, self.step_count = s["t"], s["step"]
@@ -348,12 +386,10 @@ class DistributedSimulation:
     def run_steps(self, n, check_every=16):
         if not self._prepared:
             self.prepare()
-        target = self.step_count + n
         done = 0
         while done < n:
             k = min(check_every, n - done)
-            for _ in range(k):
-                self._enqueue_step()
+            self.enqueue_steps(k)
             done += k
             s = self._sync()
             self._check(s)

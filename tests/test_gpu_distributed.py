@@ -18,8 +18,12 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("overlap", [False, True])
-def test_nccl_world1_matches_simulation(overlap):
+@pytest.mark.parametrize("overlap,graphs", [(False, False), (False, True), (True, True)])
+def test_nccl_world1_matches_simulation(overlap, graphs):
+    """NCCL world 1 (halo exchange skipped, all-reduce real): plain and
+    overlapped steps, eager and CUDA-graph-captured chunks, equal the
+    single-domain Simulation bit for bit; run_until twice and a later
+    advance() keep stepping (a reached target does not stick)."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -36,8 +40,9 @@ def test_nccl_world1_matches_simulation(overlap):
         lo, hi = stored_range(res[0], i0, i1)
         sc = build_scenario("wall-impact", res, columns=(lo, hi))
         be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
-        dsim = DistributedSimulation(be, sc.grid, overlap=overlap)
+        dsim = DistributedSimulation(be, sc.grid, overlap=overlap, graphs=graphs)
         dsim.run_steps(25, check_every=8)
+        assert dsim.use_graphs == graphs  # the capture worked
         full = build_scenario("wall-impact", res)
         sim = Simulation(full.grid, full.params, full.q0, full.boundary)
         sim.run_steps(25)
@@ -47,6 +52,15 @@ def test_nccl_world1_matches_simulation(overlap):
         dsim.run_until(t_end)
         sim.run_until(t_end)
         assert dsim.t == sim.t and np.array_equal(be.owned_state(), sim.q)
+        t_end2 = dsim.t + 3 * sim.stats.dt
+        dsim.run_until(t_end2)
+        sim.run_until(t_end2)
+        dt_d, dt_s = dsim.advance(), sim.advance()
+        assert dt_d == dt_s and dsim.step_count == sim.step_count
+        assert dsim.t == sim.t and np.array_equal(be.owned_state(), sim.q)
+        dsim.run_steps(8, check_every=8)
+        sim.run_steps(8)
+        assert np.array_equal(be.owned_state(), sim.q)
     finally:
         dist.destroy_process_group()
 
