@@ -85,6 +85,18 @@ int wb_set_stream(wb_handle* h, void* cuda_stream);
  * means q is a device pointer.  On WB_E_HEIGHT, *bad_i / *bad_j name the cell. */
 int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
                  int32_t is_device, int32_t* bad_i, int32_t* bad_j);
+/* Device-side initial condition of the detection-consistent column-equilibrium
+ * family (the dambreak / weir / wall-impact / lake configurations; scenario
+ * builders after SPEC.md:554-659, host twin: scenarios.py
+ * column_equilibrium_state): alpha = alpha_liq in the union of n_boxes
+ * (<= 8) closed rectangles {x0, x1, y0, y1} of cell centres, alpha_gas
+ * elsewhere; each column's (y0, aeq) detected from alpha as the solver
+ * detects (kernels.py:506-520); alpha*rho = aeq * eq_rho(y_c, y0)
+ * (kernels.py:53-55), or alpha * gas_rho where alpha <= 10 eps if gas_rho is
+ * not NaN; zero momenta.  Replaces wb_set_state (no host build or upload);
+ * bit-identical to the host builder. */
+int wb_init_column_equilibrium(wb_handle* h, int32_t n_boxes, const double* boxes,
+                               double alpha_liq, double alpha_gas, double gas_rho);
 /* Simulation.q read (owned columns, (i_end-i_begin, ny, 5)); solid cells come
  * back with the values uploaded for them and q[...,4] = y_centers. */
 int wb_get_state(wb_handle* h, double* q, int32_t is_device);

@@ -66,6 +66,8 @@ SIGNATURES = {
     "wb_set_state": [_H, _V, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                      ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)],
     "wb_get_state": [_H, _V, ctypes.c_int32],
+    "wb_init_column_equilibrium": [_H, ctypes.c_int32, c_double_p, ctypes.c_double,
+                                   ctypes.c_double, ctypes.c_double],
     "wb_get_state_buf": [_H, _V, ctypes.c_int32, ctypes.c_int32],
     "wb_get_cell": [_H, ctypes.c_int32, ctypes.c_int32, c_double_p],
     "wb_max_rate": [_H, c_double_p, ctypes.POINTER(WbError)],

@@ -678,6 +678,30 @@ int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
   return WB_OK;
 }
 
+int wb_init_column_equilibrium(wb_handle* h, int32_t n_boxes, const double* boxes,
+                               double alpha_liq, double alpha_gas, double gas_rho) {
+  if (!h || n_boxes < 0 || n_boxes > IC_MAX_BOXES || (n_boxes && !boxes)) {
+    g_err = "wb_init_column_equilibrium: at most 8 boxes";
+    return WB_E_ARG;
+  }
+  CK(cudaSetDevice(h->dev));
+  IcBoxes ib{};
+  ib.n = n_boxes;
+  for (int k = 0; k < n_boxes; k++)
+    for (int m = 0; m < 4; m++) ib.b[k][m] = boxes[4 * k + m];
+  ib.alpha_liq = alpha_liq;
+  ib.alpha_gas = alpha_gas;
+  k_reset_state<<<1, 1, 0, h->stream>>>(h->st, h->t, h->step);  // buffer 0 current
+  k_ic_alpha<<<148 * 8, 256, 0, h->stream>>>(h->G, h->B, ib);
+  launch_detect(h);  // (y0, aeq) of every stored column, like the solver's detection
+  k_ic_rho<<<148 * 8, 256, 0, h->stream>>>(h->G, h->B, h->P, gas_rho);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+  h->need_prepare = true;
+  h->have_state = true;
+  return WB_OK;
+}
+
 int wb_get_state(wb_handle* h, double* q, int32_t is_device) {
   return wb_get_state_buf(h, q, 0, is_device);
 }

@@ -69,7 +69,10 @@ class _CudaArray:
 class DeviceSlab:
     """Slab backend on one GPU through the C ABI (include/wbflow_b200.h)."""
 
-    def __init__(self, grid, params, q_cols, col0, boundary, cfl, i0, i1, device):
+    def __init__(self, grid, params, q_cols, col0, boundary, cfl, i0, i1, device, ic=None):
+        """q_cols: the state of the stored columns [col0, col0 + n) (host); or
+        None with ``ic`` (a scenarios.ColumnEquilibriumIC) to build this
+        slab's columns on the device (wb_init_column_equilibrium)."""
         import torch
         from . import _lib
         from .timestepper import make_config
@@ -96,10 +99,19 @@ class DeviceSlab:
         self.edge_stream = torch.cuda.Stream(device=device, priority=-1)
         _lib.check(self.L.wb_set_edge_stream(h, ctypes.c_void_p(self.edge_stream.cuda_stream)),
                    "wb_set_edge_stream")
-        q = np.ascontiguousarray(q_cols, dtype=np.float64)
-        bi, bj = ctypes.c_int32(), ctypes.c_int32()
-        _lib.check(self.L.wb_set_state(h, q.ctypes.data_as(ctypes.c_void_p), col0, q.shape[0],
-                                       0, ctypes.byref(bi), ctypes.byref(bj)), "wb_set_state")
+        if q_cols is None:
+            boxes = np.ascontiguousarray(np.array(ic.boxes, dtype=np.float64).reshape(-1))
+            _lib.check(self.L.wb_init_column_equilibrium(
+                h, len(ic.boxes), _lib.dptr(boxes) if len(ic.boxes) else None,
+                float(ic.alpha_liq), float(ic.alpha_gas),
+                math.nan if ic.gas_rho is None else float(ic.gas_rho)),
+                "wb_init_column_equilibrium")
+        else:
+            q = np.ascontiguousarray(q_cols, dtype=np.float64)
+            bi, bj = ctypes.c_int32(), ctypes.c_int32()
+            _lib.check(self.L.wb_set_state(h, q.ctypes.data_as(ctypes.c_void_p), col0,
+                                           q.shape[0], 0, ctypes.byref(bi), ctypes.byref(bj)),
+                       "wb_set_state")
         rp = ctypes.c_void_p()
         _lib.check(self.L.wb_reduce_ptr(h, ctypes.byref(rp)), "wb_reduce_ptr")
         self.red = torch.as_tensor(_CudaArray(rp.value, 2, "<i8"), device=f"cuda:{device}")

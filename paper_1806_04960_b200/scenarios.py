@@ -20,7 +20,30 @@ from .params import ModelParams
 from .state import eq_rho_profile
 
 __all__ = ["Scenario", "build_scenario", "detect_columns", "SCENARIOS",
-           "column_equilibrium_state"]
+           "column_equilibrium_state", "ColumnEquilibriumIC"]
+
+
+@dataclass
+class ColumnEquilibriumIC:
+    """The detection-consistent column-equilibrium initial condition: alpha =
+    ``alpha_liq`` in the union of ``boxes`` (closed rectangles (x0, x1, y0, y1)
+    of cell centres), ``alpha_gas`` elsewhere; liquid density from each
+    column's detected equilibrium, gas (alpha <= 10 eps) at ``gas_rho`` if
+    given; at rest.  Built on the host (``host_state``) or directly on the
+    device (``Simulation.from_scenario``, C ABI wb_init_column_equilibrium),
+    bit for bit the same."""
+    boxes: tuple
+    alpha_liq: float
+    alpha_gas: float
+    gas_rho: float = None
+
+    def host_state(self, grid, params, cols=None):
+        x, y = _centres(grid, cols)
+        liquid = np.zeros(x.shape, dtype=bool)
+        for b in self.boxes:
+            liquid |= _box(x, y, *b)
+        alpha = np.where(liquid, self.alpha_liq, self.alpha_gas)
+        return column_equilibrium_state(grid, params, alpha, cols=cols, gas_rho=self.gas_rho)
 
 
 @dataclass
@@ -29,9 +52,10 @@ class Scenario:
     grid: object
     params: ModelParams
     boundary: BoundarySpec
-    q0: np.ndarray          # (nx, ny, 5) conserved state, reference layout
+    q0: np.ndarray          # (nx, ny, 5) conserved state, reference layout (None if not built)
     t_end: float = None
     col0: int = 0           # first global column held in q0 (x-slab builds)
+    ic: ColumnEquilibriumIC = None  # device-buildable initial condition, if any
 
 
 def detect_columns(alpha, mask, y_faces, dy):
@@ -102,43 +126,36 @@ def _liquid_state(grid, params, liquid, u=None, v=None):
     return q
 
 
-def _dambreak_multi(grid, params, regions, cols=None):
-    """Dambreak with several liquid rectangles (wet bed / step cases)."""
+def _dambreak_ic(params, regions, gas_rho=None):
+    """Dambreak with one or several liquid rectangles (gas at gas_rho, default rho0)."""
     eps = params.epsilon
-    x, y = _centres(grid, cols)
-    liquid = np.zeros(x.shape, dtype=bool)
-    for r in regions:
-        liquid |= _box(x, y, *r)
-    alpha = np.where(liquid, 1.0 - eps, eps)
-    return column_equilibrium_state(grid, params, alpha, cols=cols, gas_rho=params.rho0)
+    return ColumnEquilibriumIC(tuple(tuple(float(v) for v in r) for r in regions), 1.0 - eps,
+                               eps, params.rho0 if gas_rho is None else gas_rho)
 
 
-def _dambreak(grid, params, region, gas_rho=None, cols=None):
-    eps = params.epsilon
-    x, y = _centres(grid, cols)
-    liquid = _box(x, y, *region)
-    alpha = np.where(liquid, 1.0 - eps, eps)
-    return column_equilibrium_state(grid, params, alpha, cols=cols,
-                                    gas_rho=params.rho0 if gas_rho is None else gas_rho)
+def _state(ic, grid, params, cols, host):
+    return ic.host_state(grid, params, cols) if host else None
 
 
-def _lake(name, res, obstacles, perturb_seed=None):
+def _lake(name, res, obstacles, perturb_seed=None, host=True):
     params = ModelParams(k0=2.78e5)
     grid = build_grid((-0.5, 0.5, 0.0, 1.0), res, obstacles)
-    alpha = np.ones((grid.nx, grid.ny))
-    q = column_equilibrium_state(grid, params, alpha)
-    if perturb_seed is not None:
-        rng = np.random.default_rng(perturb_seed)
-        kx, ky = rng.integers(1, 4, size=2)
-        phi = rng.uniform(0.0, 2.0 * math.pi)
-        x, y = _centres(grid)
-        rho = q[..., 0] * (1.0 + 1e-3 * np.sin(2 * math.pi * kx * x + phi)
-                           * np.cos(2 * math.pi * ky * y))
-        u = 1e-2 * np.cos(2 * math.pi * ky * y)
-        v = 1e-2 * np.sin(2 * math.pi * kx * x)
-        q[..., 0] = rho
-        q[..., 1] = rho * u
-        q[..., 2] = rho * v
+    ic = ColumnEquilibriumIC((), 1.0, 1.0, None)  # alpha = 1 everywhere
+    if perturb_seed is None:
+        return Scenario(name, grid, params, BoundarySpec(), _state(ic, grid, params, None, host),
+                        ic=ic)
+    q = ic.host_state(grid, params)
+    rng = np.random.default_rng(perturb_seed)
+    kx, ky = rng.integers(1, 4, size=2)
+    phi = rng.uniform(0.0, 2.0 * math.pi)
+    x, y = _centres(grid)
+    rho = q[..., 0] * (1.0 + 1e-3 * np.sin(2 * math.pi * kx * x + phi)
+                       * np.cos(2 * math.pi * ky * y))
+    u = 1e-2 * np.cos(2 * math.pi * ky * y)
+    v = 1e-2 * np.sin(2 * math.pi * kx * x)
+    q[..., 0] = rho
+    q[..., 1] = rho * u
+    q[..., 2] = rho * v
     return Scenario(name, grid, params, BoundarySpec(), q)
 
 
@@ -146,7 +163,7 @@ LAKE_OBSTACLES = ((-0.25, 0.25, 0.0, 0.33), (0.30, 0.40, 0.0, 0.60),
                   (-0.45, -0.35, 0.0, 0.17))
 
 
-def build_scenario(name, resolution=None, seed=0, columns=None):
+def build_scenario(name, resolution=None, seed=0, columns=None, host_state=True):
     """Build one named configuration.
 
     * ``dambreak-dry``  -- C1, [-50,50]x[0,4], liquid [-50,0]x[0,1.4618], k0 6.37e5
@@ -170,7 +187,10 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
 
     ``columns=(lo, hi)`` builds only those columns of q0 (x-slab of a
     multi-GPU run; supported by the dambreak-type scenarios); the grid is
-    always the global one.
+    always the global one.  The column-equilibrium scenarios (dambreaks, weir,
+    wall-impact, unperturbed lakes) carry ``ic``; with ``host_state=False``
+    their q0 is not built on the host (``Simulation.from_scenario`` builds it
+    on the device).
     """
     if columns is not None and name not in ("dambreak-dry", "weir", "wall-impact",
                                             "dambreak-wet", "dambreak-step-dry",
@@ -185,9 +205,10 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
         res = resolution or (200, 100)
         params = ModelParams(k0=6.37e5)
         grid = build_grid((-50.0, 50.0, 0.0, 4.0), res)
-        q = _dambreak(grid, params, (-50.0, 0.0, 0.0, 1.4618), cols=cols)
+        ic = _dambreak_ic(params, [(-50.0, 0.0, 0.0, 1.4618)])
         bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
-        return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
+        return Scenario(name, grid, params, bnd, _state(ic, grid, params, cols, host_state),
+                        col0=cols[0] if cols else 0, ic=ic)
     if name in ("dambreak-wet", "dambreak-step-dry", "dambreak-step-wet"):
         # PAPER.md section 5.6.2-5.6.4 (Omega = [-50,50]x[0,4], step [0,50]x[0,0.2])
         res = resolution or (4000, 400)
@@ -202,11 +223,12 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
             regions = [(-50.0, 0.0, 0.0, 0.4618)]
         else:
             regions = [(-50.0, 0.0, 0.0, 0.4618), (0.0, 50.0, 0.2, 0.50873)]
-        q = _dambreak_multi(grid, params, regions, cols=cols)
+        ic = _dambreak_ic(params, regions)
         bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
-        return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
+        return Scenario(name, grid, params, bnd, _state(ic, grid, params, cols, host_state),
+                        col0=cols[0] if cols else 0, ic=ic)
     if name == "equilibrium-flat":
-        return _lake(name, resolution or (100, 100), ())
+        return _lake(name, resolution or (100, 100), (), host=host_state)
     if name == "spinning-square":
         # PAPER.md section 5.3: [-5,5]^2, square [-1,1]^2, u = (2 pi y, -2 pi x), k0 8.78e5, g 0
         res = resolution or (850, 850)
@@ -231,9 +253,9 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
                            top=BoundaryCondition("transmissive"))
         return Scenario(name, grid, params, bnd, q)
     if name == "lake":
-        return _lake(name, resolution or (2048, 1024), LAKE_OBSTACLES)
+        return _lake(name, resolution or (2048, 1024), LAKE_OBSTACLES, host=host_state)
     if name == "equilibrium-obstacle":
-        return _lake(name, resolution or (100, 100), LAKE_OBSTACLES[:1])
+        return _lake(name, resolution or (100, 100), LAKE_OBSTACLES[:1], host=host_state)
     if name == "perturbed-lake":
         return _lake(name, resolution or (128, 128), LAKE_OBSTACLES, perturb_seed=seed)
     if name == "drop":
@@ -257,20 +279,23 @@ def build_scenario(name, resolution=None, seed=0, columns=None):
         params = ModelParams(k0=6.54e5)
         dx = 15.0 / res[0]
         grid = build_grid((-7.5, 7.5, 0.0, 2.1), res, [(0.0, dx, 0.0, 0.7)])
-        q = _dambreak(grid, params, (-7.5, 0.0, 0.0, 1.5), cols=cols)
-        return Scenario(name, grid, params, BoundarySpec(), q, col0=cols[0] if cols else 0)
+        ic = _dambreak_ic(params, [(-7.5, 0.0, 0.0, 1.5)])
+        return Scenario(name, grid, params, BoundarySpec(),
+                        _state(ic, grid, params, cols, host_state),
+                        col0=cols[0] if cols else 0, ic=ic)
     if name == "wall-impact":
         res = resolution or (32768, 16384)
         params = ModelParams(k0=2.62e5)
         grid = build_grid((0.0, 3.2, 0.0, 1.8), res)
-        q = _dambreak(grid, params, (0.0, 1.2, 0.0, 0.6), cols=cols)
+        ic = _dambreak_ic(params, [(0.0, 1.2, 0.0, 0.6)])
         bnd = BoundarySpec(top=BoundaryCondition("transmissive"))
-        return Scenario(name, grid, params, bnd, q, col0=cols[0] if cols else 0)
+        return Scenario(name, grid, params, bnd, _state(ic, grid, params, cols, host_state),
+                        col0=cols[0] if cols else 0, ic=ic)
     if name == "jet":
         res = resolution or (96, 64)
         params = ModelParams(k0=2.78e5, g=9.81)
         grid = build_grid((0.0, 3.0, 0.0, 2.0), res, [(1.8, 2.1, 0.0, 0.9)])
-        q = _dambreak(grid, params, (0.0, 0.6, 0.0, 0.5))
+        q = _dambreak_ic(params, [(0.0, 0.6, 0.0, 0.5)]).host_state(grid, params)
         eps = params.epsilon
         state = (params.rho0, 2.0, 0.0, 1.0 - eps, 0.0)
         bnd = BoundarySpec(left=BoundaryCondition("inflow", state, (0.2, 0.6)),

@@ -89,7 +89,7 @@ class Simulation:
     """Device-resident double-buffered simulation (timestepper.py:48-103)."""
 
     def __init__(self, grid, params, q0, boundary=None, cfl=0.45, workers=1, device=0,
-                 debug=False, rows_per_block=0):
+                 debug=False, rows_per_block=0, device_ic=None):
         if not 0.0 < cfl < 1.0:
             raise SimulationError(f"cfl must lie in (0, 1), got {cfl}")
         self.grid = grid
@@ -101,9 +101,12 @@ class Simulation:
         self.device = int(device)
         set_workers(workers)
         nx, ny = grid.nx, grid.ny
-        q0 = np.asarray(q0, dtype=np.float64)
-        if q0.shape != (nx, ny, 5):
-            raise SimulationError(f"q0 must have shape {(nx, ny, 5)}, got {q0.shape}")
+        if q0 is None and device_ic is None:
+            raise SimulationError("q0 is required (or a device-buildable initial condition)")
+        if q0 is not None:
+            q0 = np.asarray(q0, dtype=np.float64)
+            if q0.shape != (nx, ny, 5):
+                raise SimulationError(f"q0 must have shape {(nx, ny, 5)}, got {q0.shape}")
         self._L = _lib.load()
         self._fluid = np.asarray(grid.mask) != 0
         # flat indices of the solid cells (usually none): a boolean-mask gather
@@ -126,7 +129,10 @@ class Simulation:
         self._edges = None
         self._qh = None           # cached host mirror of the current state
         self._qh_exposed = False  # handed out by the q property (may be written)
-        self._set_q(q0)
+        if q0 is not None:
+            self._set_q(q0)
+        else:
+            self._init_on_device(device_ic)
         if self.debug:
             for name in ("fW", "fE", "fS", "fN", "vol", "psi", "DW", "DE", "DS", "DN"):
                 setattr(self, name, np.zeros((nx, ny, 5)))
@@ -165,9 +171,39 @@ class Simulation:
         q = out if out is not None else np.empty((nx, ny, 5))
         check(self._L.wb_get_state_buf(self._h, q.ctypes.data_as(ctypes.c_void_p), which, 0),
               "wb_get_state")
-        if self._solid_flat.size:
+        if self._solid_flat.size and self._solid_q is not None:
             q.reshape(-1, 5)[self._solid_flat] = self._solid_q
         return q
+
+    @classmethod
+    def from_scenario(cls, sc, cfl=0.45, device=0, debug=False, rows_per_block=0,
+                      device_ic=True):
+        """Simulation of a ``scenarios.Scenario``.  A column-equilibrium initial
+        condition (``sc.ic``) is built directly on the device -- no host q0,
+        no upload (``build_scenario(..., host_state=False)`` skips the host
+        build too); anything else uploads ``sc.q0``."""
+        if device_ic and sc.ic is not None:
+            return cls(sc.grid, sc.params, None, sc.boundary, cfl=cfl, device=device,
+                       debug=debug, rows_per_block=rows_per_block, device_ic=sc.ic)
+        if sc.q0 is None:
+            raise SimulationError(f"scenario {sc.name!r} has no host state")
+        return cls(sc.grid, sc.params, sc.q0, sc.boundary, cfl=cfl, device=device, debug=debug,
+                   rows_per_block=rows_per_block)
+
+    def _init_on_device(self, ic):
+        """The column-equilibrium initial condition built by the device
+        (wb_init_column_equilibrium, bit-identical to ic.host_state)."""
+        boxes = np.ascontiguousarray(np.array(ic.boxes, dtype=np.float64).reshape(-1))
+        gas = math.nan if ic.gas_rho is None else float(ic.gas_rho)
+        check(self._L.wb_init_column_equilibrium(
+            self._h, len(ic.boxes), dptr(boxes) if len(ic.boxes) else None,
+            float(ic.alpha_liq), float(ic.alpha_gas), gas), "wb_init_column_equilibrium")
+        self._qh = None
+        self._qh_exposed = False
+        # host copies of the (unchanging) solid cells, for sim.q downloads
+        self._solid_q = None
+        if self._solid_flat.size:
+            self._solid_q = self._get_q(0).reshape(-1, 5)[self._solid_flat].copy()
 
     def _host_q(self):
         """The current state on the host (cached until the next step)."""

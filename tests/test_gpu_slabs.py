@@ -20,15 +20,16 @@ def torch_cuda():
     return torch
 
 
-def _slabs(torch, scen, res, world):
+def _slabs(torch, scen, res, world, device_ic=False):
     from paper_1806_04960_b200.distributed import DeviceSlab, slab_bounds, stored_range
     from paper_1806_04960_b200.scenarios import build_scenario
     out = []
     for r in range(world):
         i0, i1 = slab_bounds(res[0], world, r)
         lo, hi = stored_range(res[0], i0, i1)
-        sc = build_scenario(scen, res, columns=(lo, hi))
-        out.append(DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0))
+        sc = build_scenario(scen, res, columns=(lo, hi), host_state=not device_ic)
+        out.append(DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0,
+                              ic=sc.ic if device_ic else None))
     return out
 
 

@@ -44,3 +44,4 @@ def test_timeseries_rows():
         rows = open(path).read().splitlines()
         assert rows[0] == "step,t,dt,mass,max_rate,cells_per_second,E_rho"
         assert rows[1].split(",")[3] == "12.5" and rows[2].split(",")[3] == "12.25"
+
