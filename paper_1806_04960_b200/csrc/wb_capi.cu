@@ -271,16 +271,19 @@ static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
   const Geo& G = h->G;
   const int nt = step_nt(h, DEBUG);
   dim3 g = step_grid(h, nt);
-  Part part{0, 1, 0};
+  Part part{0, 1, 0, 0};
   // the edge launch must produce both halo-source column pairs: split only if
   // there is an interior strip and the last strip owns at least HALO columns
   const bool split = g.x >= 3 && h->G.nxl - ((int)g.x - 1) * (nt - 2 * HALO) >= HALO;
   if (which == PART_EDGE) {
-    part = split ? Part{0, (int)g.x - 1, 1} : Part{0, 1, 1};
+    // split: the edge strips detect their columns with k_detect_cols (a
+    // 256-link fused chain over two strips would be the edge stream's
+    // critical path); unsplit, this launch is the whole step and fuses it
+    part = split ? Part{0, (int)g.x - 1, 1, 1} : Part{0, 1, 1, 0};
     if (split) g.x = 2;
   } else if (which == PART_INTERIOR) {
     if (!split) return;
-    part = Part{1, 1, 0};
+    part = Part{1, 1, 0, 0};
     g.x -= 2;
   }
 #define WB_LAUNCH(K, NTV)                                                          \
@@ -1126,6 +1129,19 @@ int wb_step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void*
   CK(cudaEventRecord(h->ev_fork, h->stream));
   CK(cudaStreamWaitEvent(h->edge, h->ev_fork, 0));
   launch_step<false>(h, Dbg{}, h->edge, PART_EDGE);
+  {
+    // a split edge launch leaves the detection of its strips' owned columns
+    // to k_detect_cols (see launch_step); the pack needs it for the halo
+    const int nt = step_nt(h, false), w = nt - 2 * HALO;
+    const dim3 g = step_grid(h, nt);
+    const bool split = g.x >= 3 && h->G.nxl - ((int)g.x - 1) * w >= HALO;
+    if (split && h->B.fuse_detect) {
+      const int c0 = HALO, c1 = std::min(HALO + w, h->G.nxl + HALO);
+      const int c2 = ((int)g.x - 1) * w + HALO, c3 = std::min(c2 + w, h->G.nxl + HALO);
+      const int ncols = (c1 - c0) + (c3 - c2);
+      k_detect_cols<<<(ncols + 7) / 8, 256, 0, h->edge>>>(h->G, h->B, h->P.dy, c0, c1, c2, c3);
+    }
+  }
   k_pack_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, (double*)send, 1);
   launch_step<false>(h, Dbg{}, h->stream, PART_INTERIOR);
   CK(cudaGetLastError());

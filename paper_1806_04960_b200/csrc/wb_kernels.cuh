@@ -76,6 +76,7 @@ struct Bufs {
 // -- slab-edge strips and interior strips -- run concurrently)
 struct Part {
   int bx0, bxs, tslot;
+  int nofuse;  // 1: this launch leaves the detection of q^{n+1} to k_detect_cols
 };
 struct Dbg {
   double *fW, *fE, *fS, *fN, *vol, *psi, *DW, *DE, *DS, *DN;

@@ -214,7 +214,7 @@ class DistributedSimulation:
     torch.distributed process group (the reference's Simulation semantics:
     same dt sequence, same error step/cell, bit-identical state)."""
 
-    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=False, graphs=True):
+    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=True, graphs=True):
         import torch.distributed as dist
         self.dist = dist
         self.be = backend
@@ -227,12 +227,12 @@ class DistributedSimulation:
         self.step_count = 0
         self._prepared = False
         self._nccl = dist.get_backend(group) == "nccl"
-        # overlapped step: edge strips + halo exchange on the backend's edge
-        # stream while the interior strips run (SURVEY.md 8(e) "Overlap").
-        # Off by default: measured on one B200 (tools/overlap_bench.py, C5
-        # slab) the split costs ~0.5 ms per step -- the edge launch's fused
-        # detection chain runs its 256 row segments back to back -- against
-        # ~0.05 ms of exchange it could hide.
+        # overlapped step (default): edge strips + halo exchange on the
+        # backend's edge stream while the interior strips run (SURVEY.md 8(e)
+        # "Overlap").  The edge strips detect their columns with a one-warp-
+        # per-column kernel instead of the fused chain, so on one B200 the
+        # split step costs the same as the plain one (6.654 vs 6.658 ms on the
+        # C5 slab, tools/overlap_bench.py) and hides the exchange on several.
         self.overlap = overlap and hasattr(backend, "step_begin")
         # device loops over NCCL are captured once per chunk length as a CUDA
         # graph (kernels + collectives), replayed without host enqueue work;

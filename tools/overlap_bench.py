@@ -24,20 +24,26 @@ res = (4096, 16384)
 i0, i1 = slab_bounds(res[0], 1, 0)
 lo, hi = stored_range(res[0], i0, i1)
 sc = build_scenario("wall-impact", res, columns=(lo, hi))
-for overlap in (False, True, False, True):
-    be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
-    sim = DistributedSimulation(be, sc.grid, overlap=overlap)
-    sim.run_steps(3)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(be.stream)
-    for _ in range(steps):
-        sim._enqueue_step()
-    e1.record(be.stream)
-    torch.cuda.synchronize()
-    st = sim._sync()
-    sim._check(st)
-    print(f"overlap={overlap}: {e0.elapsed_time(e1) / steps:.3f} ms/step", flush=True)
-    del sim, be
-    torch.cuda.empty_cache()
+import hashlib  # noqa: E402
+digests = set()
+for rnd in range(2):
+    for overlap, graphs in ((False, False), (True, False), (False, True), (True, True)):
+        be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
+        sim = DistributedSimulation(be, sc.grid, overlap=overlap, graphs=graphs)
+        sim.run_steps(3)
+        sim.enqueue_steps(steps)  # captures the graph (graphs=True) outside the timing
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(be.stream)
+        sim.enqueue_steps(steps)
+        e1.record(be.stream)
+        torch.cuda.synchronize()
+        st = sim._sync()
+        sim._check(st)
+        digests.add(hashlib.sha256(be.owned_state().tobytes()).hexdigest()[:16])
+        print(f"overlap={overlap} graphs={graphs and sim.use_graphs}: "
+              f"{e0.elapsed_time(e1) / steps:.3f} ms/step", flush=True)
+        del sim, be
+        torch.cuda.empty_cache()
+print("states", "IDENTICAL" if len(digests) == 1 else f"DIFFER {digests}")
 dist.destroy_process_group()
