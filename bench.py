@@ -34,6 +34,23 @@ SLAB = (4096, 16384)
 HBM_BYTES_PER_CELL = 64.0  # read 4 + write 4 FP64 dynamic components
 
 
+def committed_traffic(nx, ny):
+    """DRAM bytes per k_step launch and the ncu counters of the committed
+    capture (profiles/kstep_traffic.json) when it was taken on this slab shape
+    (an N-rank run's per-rank slab has the N = 1 shape)."""
+    tpath = os.path.join(ROOT, "profiles", "kstep_traffic.json")
+    if not os.path.exists(tpath):
+        return None, None
+    with open(tpath) as f:
+        tj = json.load(f)
+    if tj.get("grid") != [nx, ny]:
+        return None, None
+    ncu = {k: tj.get(k) for k in ("fp64_pipe_active_pct", "issue_active_pct",
+                                   "warps_per_sm", "registers_per_thread")}
+    ncu["source"] = tj.get("source")
+    return tj.get("dram_bytes_per_launch"), ncu
+
+
 def flops_per_step(n_fluid, n2nd, ex, ey):
     """Algorithmic FP64 work of one step (dynamic counts of
     the reference code paths)."""
@@ -294,17 +311,7 @@ def run_ours(args):
     hbm_achieved = HBM_BYTES_PER_CELL * n_fluid / (mst.value * 1e-3) / 1e9
     t_hbm = HBM_BYTES_PER_CELL * n_fluid / (hbm_peak * 1e9)
     t_fp64 = F / (tf.value * 1e12)
-    traffic = None
-    ncu = None
-    tpath = os.path.join(ROOT, "profiles", "kstep_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tj = json.load(f)
-        if tj.get("grid") == [nx, ny]:
-            traffic = tj.get("dram_bytes_per_launch")
-            ncu = {k: tj.get(k) for k in ("fp64_pipe_active_pct", "issue_active_pct",
-                                           "warps_per_sm", "registers_per_thread")}
-            ncu["source"] = tj.get("source")
+    traffic, ncu = committed_traffic(nx, ny)
     roof = {"bound": "fp64" if t_fp64 >= t_hbm else "hbm",
             "achieved": fp64_achieved if t_fp64 >= t_hbm else hbm_achieved,
             "peak": tf.value if t_fp64 >= t_hbm else hbm_peak,
@@ -464,7 +471,7 @@ def run_ours_distributed(args):
     if rank == 0:
         state_bytes = sc.q0.nbytes * world
         roof = {"bound": "fp64", "achieved": fp64, "peak": tf.value, "unit": "TFLOP/s",
-                "frac": fp64 / tf.value, "traffic": None,
+                "frac": fp64 / tf.value, "traffic": committed_traffic(*slab())[0],
                 "kernel": "k_step on rank 0's slab, timed alone (wb_profile_steps)",
                 "kernel_ms": mst.value, "flop_per_step": F,
                 "counters": {"n_second_order": n2, "x_faces": ex, "y_faces": ey,

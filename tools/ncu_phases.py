@@ -86,7 +86,8 @@ def main(mix, dis, name=KERNEL, src=SRC):
                 for ln, nm in marks:
                     if ln <= inner[-1]:
                         ph = nm
-        x = acc.setdefault(ph, [0, 0, 0, {}])
+        x = acc.setdefault(ph, [0, 0, 0, {}, 0])
+        x[4] += 1  # static SASS size (16 B per instruction)
         x[0] += s
         x[1] += e
         x[2] += th
@@ -94,12 +95,12 @@ def main(mix, dis, name=KERNEL, src=SRC):
             x[3][k] = x[3].get(k, 0) + v
     ts = sum(v[0] for v in acc.values()) or 1
     te = sum(v[1] for v in acc.values()) or 1
-    print("| phase | warp-instructions | stall samples | threads/instr | top stall reasons |")
-    print("|---|---|---|---|---|")
+    print("| phase | code KB | warp-instructions | stall samples | threads/instr | top stall reasons |")
+    print("|---|---|---|---|---|---|")
     for k, v in sorted(acc.items(), key=lambda x: -x[1][0]):
         top = sorted(v[3].items(), key=lambda x: -x[1])[:3]
         tops = ", ".join(f"{n[6:]} {100 * c / max(1, v[0]):.0f}%" for n, c in top)
-        print(f"| {k} | {100 * v[1] / te:.1f}% | {100 * v[0] / ts:.1f}% | "
+        print(f"| {k} | {v[4] * 16 / 1024:.1f} | {100 * v[1] / te:.1f}% | {100 * v[0] / ts:.1f}% | "
               f"{v[2] / max(1, v[1]):.1f} | {tops} |")
 
 

@@ -1,7 +1,7 @@
 """Copy the round's measurement artefacts from gpurun_out/ into profiles/.
 
-python tools/summarize_profiles.py ROUND NCU_REP
-Writes profiles/rROUND_launches_bench.csv, rROUND_kstep_ncu_raw_selected.csv,
+python tools/summarize_profiles.py ROUND NCU_REP [LAUNCHES_CSV BENCH_JSON]
+(defaults gpurun_out/launches_r01.csv, gpurun_out/bench_full.json).  Writes profiles/rROUND_launches_bench.csv, rROUND_kstep_ncu_raw_selected.csv,
 kstep_traffic.json and prints the launch table (markdown)."""
 import collections
 import csv
@@ -13,11 +13,11 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rnd, rep = sys.argv[1], sys.argv[2]
+launches = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out", "launches_r01.csv")
+bench = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "gpurun_out", "bench_full.json")
 prof = os.path.join(ROOT, "profiles")
-shutil.copy(os.path.join(ROOT, "gpurun_out", "launches_r01.csv"),
-            os.path.join(prof, f"r{rnd}_launches_bench.csv"))
-shutil.copy(os.path.join(ROOT, "gpurun_out", "bench_full.json"),
-            os.path.join(prof, f"r{rnd}_bench.json"))
+shutil.copy(launches, os.path.join(prof, f"r{rnd}_launches_bench.csv"))
+shutil.copy(bench, os.path.join(prof, f"r{rnd}_bench.json"))
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout.splitlines()
 rows = list(csv.reader(raw))
