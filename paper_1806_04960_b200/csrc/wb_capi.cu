@@ -90,6 +90,10 @@ struct wb_handle {
   bool own_stream = false;
   cudaStream_t edge = nullptr;  // slab-edge strips + halo exchange (wb_set_edge_stream)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // host transfers: copies on their own stream, double-buffered staging, so
+  // the copy of one column chunk overlaps the layout transpose of the other
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t ev_x0 = nullptr, ev_copy[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   double* planes = nullptr;
   uint8_t* mask = nullptr;
   // TMA descriptors of the plane stack and the mask, one pair per CTA width
@@ -127,13 +131,23 @@ static int chunk_cols(int ny) {
   return (int)c;
 }
 
+// two staging buffers of `bytes` each (h->tmp, h->tmp + bytes) and the
+// transfer stream / events
 static int ensure_tmp(wb_handle* h, size_t bytes) {
-  if (h->tmp_bytes >= bytes) return WB_OK;
+  if (!h->xfer) {
+    CK(cudaStreamCreateWithFlags(&h->xfer, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_x0, cudaEventDisableTiming));
+    for (int b = 0; b < 2; b++) {
+      CK(cudaEventCreateWithFlags(&h->ev_copy[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_used[b], cudaEventDisableTiming));
+    }
+  }
+  if (h->tmp_bytes >= 2 * bytes) return WB_OK;
   if (h->tmp) cudaFree(h->tmp);
   h->tmp = nullptr;
   h->tmp_bytes = 0;
-  CK(cudaMalloc(&h->tmp, bytes));
-  h->tmp_bytes = bytes;
+  CK(cudaMalloc(&h->tmp, 2 * bytes));
+  h->tmp_bytes = 2 * bytes;
   return WB_OK;
 }
 
@@ -613,6 +627,14 @@ int wb_destroy(wb_handle* h) {
   cudaFree(h->dtlog);
   cudaFree(h->scratch);
   if (h->tmp) cudaFree(h->tmp);
+  if (h->xfer) {
+    cudaStreamDestroy(h->xfer);
+    cudaEventDestroy(h->ev_x0);
+    for (int b = 0; b < 2; b++) {
+      cudaEventDestroy(h->ev_copy[b]);
+      cudaEventDestroy(h->ev_used[b]);
+    }
+  }
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -649,19 +671,27 @@ int wb_set_state(wb_handle* h, const double* q, int32_t i_first, int32_t n_cols,
     k_aos_to_planes<<<dim3((n_cols + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0,
                       h->stream>>>(h->G, h->B, q, i_first, n_cols, h->scratch);
   } else {
-    // host source: column chunks through one device staging buffer (stream
-    // order makes the reuse safe), so an upload needs ~128 MB of scratch
-    // instead of a full 40 B/cell AoS copy on the device
+    // host source: column chunks through two ~128 MB device staging buffers
+    // (instead of a full 40 B/cell AoS copy on the device); chunk i is copied
+    // on the transfer stream into buffer i % 2 once the transpose of chunk
+    // i - 2 has released it, and transposed on the handle's stream once copied
     const int ch = chunk_cols(G.ny);
-    int rc = ensure_tmp(h, (size_t)ch * G.ny * 5 * sizeof(double));
+    const size_t cb = (size_t)ch * G.ny * 5;
+    int rc = ensure_tmp(h, cb * sizeof(double));
     if (rc) return rc;
-    for (int k = 0; k < n_cols; k += ch) {
-      const int nk = std::min(ch, n_cols - k);
-      CK(cudaMemcpyAsync(h->tmp, q + (size_t)k * G.ny * 5,
-                         (size_t)nk * G.ny * 5 * sizeof(double), cudaMemcpyHostToDevice,
-                         h->stream));
+    CK(cudaEventRecord(h->ev_x0, h->stream));
+    CK(cudaStreamWaitEvent(h->xfer, h->ev_x0, 0));
+    for (int k = 0, i = 0; k < n_cols; k += ch, i++) {
+      const int nk = std::min(ch, n_cols - k), b = i & 1;
+      double* buf = h->tmp + b * cb;
+      if (i >= 2) CK(cudaStreamWaitEvent(h->xfer, h->ev_used[b], 0));
+      CK(cudaMemcpyAsync(buf, q + (size_t)k * G.ny * 5, (size_t)nk * G.ny * 5 * sizeof(double),
+                         cudaMemcpyHostToDevice, h->xfer));
+      CK(cudaEventRecord(h->ev_copy[b], h->xfer));
+      CK(cudaStreamWaitEvent(h->stream, h->ev_copy[b], 0));
       k_aos_to_planes<<<dim3((nk + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
-          h->G, h->B, h->tmp, i_first + k, nk, h->scratch);
+          h->G, h->B, buf, i_first + k, nk, h->scratch);
+      CK(cudaEventRecord(h->ev_used[b], h->stream));
     }
   }
   CK(cudaGetLastError());
@@ -718,17 +748,26 @@ int wb_get_state_buf(wb_handle* h, double* q, int32_t which, int32_t is_device) 
     k_planes_to_aos<<<dim3((G.nxl + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
         G, h->B, q, which ? 1 : -1, 0, G.nxl);
   } else {
+    // column chunks: transposed on the handle's stream into staging buffer
+    // i % 2 (once the copy of chunk i - 2 has released it), copied out on the
+    // transfer stream
     const int ch = chunk_cols(G.ny);
-    int rc = ensure_tmp(h, (size_t)ch * G.ny * 5 * sizeof(double));
+    const size_t cb = (size_t)ch * G.ny * 5;
+    int rc = ensure_tmp(h, cb * sizeof(double));
     if (rc) return rc;
-    for (int k = 0; k < G.nxl; k += ch) {
-      const int nk = std::min(ch, G.nxl - k);
+    for (int k = 0, i = 0; k < G.nxl; k += ch, i++) {
+      const int nk = std::min(ch, G.nxl - k), b = i & 1;
+      double* buf = h->tmp + b * cb;
+      if (i >= 2) CK(cudaStreamWaitEvent(h->stream, h->ev_copy[b], 0));
       k_planes_to_aos<<<dim3((nk + TT - 1) / TT, (G.ny + TT - 1) / TT), 256, 0, h->stream>>>(
-          G, h->B, h->tmp, which ? 1 : -1, k, nk);
-      CK(cudaMemcpyAsync(q + (size_t)k * G.ny * 5, h->tmp,
-                         (size_t)nk * G.ny * 5 * sizeof(double), cudaMemcpyDeviceToHost,
-                         h->stream));
+          G, h->B, buf, which ? 1 : -1, k, nk);
+      CK(cudaEventRecord(h->ev_used[b], h->stream));
+      CK(cudaStreamWaitEvent(h->xfer, h->ev_used[b], 0));
+      CK(cudaMemcpyAsync(q + (size_t)k * G.ny * 5, buf, (size_t)nk * G.ny * 5 * sizeof(double),
+                         cudaMemcpyDeviceToHost, h->xfer));
+      CK(cudaEventRecord(h->ev_copy[b], h->xfer));
     }
+    CK(cudaStreamSynchronize(h->xfer));
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
