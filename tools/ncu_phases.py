@@ -14,7 +14,8 @@ import csv
 import re
 import sys
 
-KERNEL = "_ZN2wb6k_stepILi64ELi1ELb1ELb0EEEvNS_3GeoENS_4BufsENS_4PhysEiNS_3DbgE"
+KERNEL = ("_ZN2wb6k_stepILi128ELi3ELb1ELb0EEEvNS_3GeoENS_4BufsENS_4PhysEiNS_3DbgENS_4PartE"
+          "14CUtensorMap_stS6_")  # the default launch on large grids
 SRC = "paper_1806_04960_b200/csrc/wb_step.cu"
 
 
