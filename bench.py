@@ -430,6 +430,7 @@ def run_ours_distributed(args):
     for _ in range(args.steps // chunk):
         sim.enqueue_steps(chunk)
     graphs_used = sim.use_graphs
+    halo_mode, overlapped = sim.halo, sim.overlap
     e1.record(be.stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -481,12 +482,16 @@ def run_ours_distributed(args):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PUBLISHED,
                 "dtype": "f64", "data": "synthetic",
                 "config": bench_config(nx, ny, n_fluid, world),
-                "parallelism": f"x-slab dp{world}, {backend} halo send/recv + one "
-                               "MAX all-reduce per step"
+                "parallelism": f"x-slab dp{world}, "
+                               + ("halo stored into the neighbours over peer memory (CUDA IPC)"
+                                  if halo_mode == "peer" else f"{backend} halo send/recv")
+                               + f" + one {backend} MAX all-reduce per step"
+                               + (", edge strips overlapped" if overlapped else "")
                                + (", CUDA graph of the step sequence" if graphs_used else ""),
-                # per step: set_run, reset_counters, k_step, prefinalize, finalize,
-                # pack_halo, unpack_halo
-                "gpu_launches": 7 * args.steps,
+                # per overlapped step: set_run, reset_counters, k_step (edge strips),
+                # k_detect_cols, k_step (interior), prefinalize, finalize, and the
+                # halo: k_push_halo (peer) or k_pack_halo + k_unpack_halo
+                "gpu_launches": (8 if halo_mode == "peer" else 9) * args.steps,
                 "roofline": roof, "cpu_baseline": None,
                 "e2e": {"value": n_fluid * args.steps / wall, "unit": UNIT,
                         "h2d_bytes_per_step": state_bytes / args.steps,

@@ -182,6 +182,39 @@ int wb_unpack_halo_next(wb_handle* h, const void* recv_dev, int32_t have_left,
                         int32_t have_right);
 int wb_step_end(wb_handle* h);
 
+/* Halo over peer memory (replaces the pack -> NCCL
+ * send/recv -> unpack of the exchange above): the slab's new boundary columns
+ * are stored by one kernel straight into the x-neighbours' halo columns of
+ * their step output buffer -- NVLink/NVSwitch stores to another GPU's HBM, or
+ * plain stores for another slab on the same GPU.  A wb_peer describes a
+ * slab's buffers as pointers valid on the calling handle's device. */
+typedef struct {
+  void* q[2][4];      /* state planes [buffer][component], index j*pitch + c */
+  void* y0s[2];       /* per stored column, detection of buffer b */
+  void* aeqs[2];
+  int32_t pitch, nxl, ny, pad;
+} wb_peer;
+/* this handle's own buffers (for a peer in the same process) */
+int wb_peer_desc(wb_handle* h, wb_peer* out);
+/* export this handle's buffers for another process (cudaIpcGetMemHandle):
+ * writes WB_PEER_IPC_BYTES bytes to blob */
+#define WB_PEER_IPC_BYTES 256
+int wb_peer_ipc_export(wb_handle* h, void* blob);
+/* open another process's exported buffers on this handle's device (closed by
+ * wb_destroy) */
+int wb_peer_ipc_open(wb_handle* h, const void* blob, wb_peer* out);
+/* the left / right x-neighbour (NULL: none; peer access is enabled when a
+ * peer lives on another device) */
+int wb_set_peers(wb_handle* h, const wb_peer* left, const wb_peer* right);
+/* wb_step_begin with the halo stored into the peers instead of packed: then
+ * wb_step_end -> all-reduce -> wb_finalize.  The all-reduce orders the peer
+ * stores before any rank's next step, and no rank stores into a buffer a
+ * neighbour still reads (the halo goes to the step's output buffer). */
+int wb_step_begin_peer(wb_handle* h, double max_dt, double t_end, int32_t mode);
+/* the plain step's counterpart: wb_step_local -> wb_push_halo_next ->
+ * all-reduce -> wb_finalize */
+int wb_push_halo_next(wb_handle* h);
+
 /* ---- measurement ---- */
 /* n steps launched one by one with CUDA events on the handle's stream:
  * average device time of the detection kernel, the fused step kernel and the

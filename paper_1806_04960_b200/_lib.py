@@ -49,6 +49,16 @@ class WbStatus(ctypes.Structure):
                 ("replays_by_kind", ctypes.c_uint64 * 6)]
 
 
+class WbPeer(ctypes.Structure):
+    """wb_peer: an x-neighbour slab's buffers as pointers on this device."""
+    _fields_ = [("q", (ctypes.c_void_p * 4) * 2), ("y0s", ctypes.c_void_p * 2),
+                ("aeqs", ctypes.c_void_p * 2), ("pitch", ctypes.c_int32),
+                ("nxl", ctypes.c_int32), ("ny", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+WB_PEER_IPC_BYTES = 256
+
+
 class WbStageArrays(ctypes.Structure):
     _fields_ = [(n, c_double_p) for n in ("fW", "fE", "fS", "fN", "vol", "psi", "DW", "DE",
                                           "DS", "DN", "rhoE_c", "rhoE_fy")] + \
@@ -97,6 +107,12 @@ SIGNATURES = {
     "wb_step_begin": [_H, ctypes.c_double, ctypes.c_double, ctypes.c_int32, _V],
     "wb_unpack_halo_next": [_H, _V, ctypes.c_int32, ctypes.c_int32],
     "wb_step_end": [_H],
+    "wb_peer_desc": [_H, ctypes.POINTER(WbPeer)],
+    "wb_peer_ipc_export": [_H, _V],
+    "wb_peer_ipc_open": [_H, _V, ctypes.POINTER(WbPeer)],
+    "wb_set_peers": [_H, ctypes.POINTER(WbPeer), ctypes.POINTER(WbPeer)],
+    "wb_step_begin_peer": [_H, ctypes.c_double, ctypes.c_double, ctypes.c_int32],
+    "wb_push_halo_next": [_H],
     "wb_eval_faces": [_H, ctypes.c_int32, ctypes.c_int64, _V, _V, _V, _V, _V],
     "wb_depth_averaged_velocity": [_H, _V],
     "wb_sync": [_H],

@@ -121,6 +121,11 @@ struct wb_handle {
   cudaGraphExec_t graph = nullptr;
   int graph_chunk = 0;
   int variant = 0;  // k_step launch configuration (auto, or WB_KSTEP_VARIANT)
+  // halo over peer memory: the x-neighbours' buffers, and the allocations of
+  // other processes opened here (closed by wb_destroy)
+  PeerBufs peer[2] = {};
+  void* ipc_open[6] = {};
+  int n_ipc_open = 0;
 };
 
 // columns per host-transfer chunk: ~128 MB of AoS, a multiple of the
@@ -635,6 +640,7 @@ int wb_destroy(wb_handle* h) {
       cudaEventDestroy(h->ev_used[b]);
     }
   }
+  for (int k = 0; k < h->n_ipc_open; k++) cudaIpcCloseMemHandle(h->ipc_open[k]);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -1155,8 +1161,17 @@ int wb_set_edge_stream(wb_handle* h, void* s) {
 // their new halo-source columns (from the step's output buffer) into `send`.
 // The caller exchanges `send`/`recv` on the edge stream, calls
 // wb_unpack_halo_next there, then wb_step_end.
+static int step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void* send);
 int wb_step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void* send) {
   if (!h || !send) return WB_E_ARG;
+  return step_begin(h, max_dt, t_end, mode, send);
+}
+int wb_step_begin_peer(wb_handle* h, double max_dt, double t_end, int32_t mode) {
+  if (!h) return WB_E_ARG;
+  return step_begin(h, max_dt, t_end, mode, nullptr);
+}
+// send == nullptr: store the halo into the peers (k_push_halo), else pack it
+static int step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void* send) {
   if (!h->have_state) return WB_E_STATE;
   if (!h->edge) return WB_E_STATE;
   CK(cudaSetDevice(h->dev));
@@ -1181,7 +1196,10 @@ int wb_step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, void*
       k_detect_cols<<<(ncols + 7) / 8, 256, 0, h->edge>>>(h->G, h->B, h->P.dy, c0, c1, c2, c3);
     }
   }
-  k_pack_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, (double*)send, 1);
+  if (send)
+    k_pack_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, (double*)send, 1);
+  else if (h->peer[0].q[0][0] || h->peer[1].q[0][0])
+    k_push_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, h->peer[0], h->peer[1], 1);
   launch_step<false>(h, Dbg{}, h->stream, PART_INTERIOR);
   CK(cudaGetLastError());
   return WB_OK;
@@ -1204,6 +1222,120 @@ int wb_step_end(wb_handle* h) {
   CK(cudaGetLastError());
   return WB_OK;
 }
+// ---- halo over peer memory ----
+namespace {
+struct PeerIpc {  // WB_PEER_IPC_BYTES bytes
+  cudaIpcMemHandle_t planes, y0s, aeqs;  // 3 x 64 bytes
+  long long plane, shift;                // doubles per plane, PLANE_SHIFT
+  int pitch, nxl, ny, magic;
+  char pad[WB_PEER_IPC_BYTES - 3 * sizeof(cudaIpcMemHandle_t) - 2 * sizeof(long long) -
+           4 * sizeof(int)];
+};
+static_assert(sizeof(PeerIpc) == WB_PEER_IPC_BYTES, "peer IPC blob size");
+constexpr int PEER_MAGIC = 0x57425032;  // "WBP2"
+void fill_peer(wb_peer* out, double* planes, double* y0s, double* aeqs, long long plane,
+               long long shift, int pitch, int nxl, int ny) {
+  memset(out, 0, sizeof(*out));
+  for (int b = 0; b < 2; b++) {
+    for (int m = 0; m < 4; m++) out->q[b][m] = planes + shift + (b * 4 + m) * plane;
+    out->y0s[b] = y0s + b * pitch;
+    out->aeqs[b] = aeqs + b * pitch;
+  }
+  out->pitch = pitch;
+  out->nxl = nxl;
+  out->ny = ny;
+}
+}  // namespace
+
+int wb_peer_desc(wb_handle* h, wb_peer* out) {
+  if (!h || !out) return WB_E_ARG;
+  fill_peer(out, h->planes, h->y0s, h->aeqs, (long long)h->G.pitch * h->G.ny, PLANE_SHIFT,
+            h->G.pitch, h->G.nxl, h->G.ny);
+  return WB_OK;
+}
+int wb_peer_ipc_export(wb_handle* h, void* blob) {
+  if (!h || !blob) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  PeerIpc p;
+  memset(&p, 0, sizeof(p));
+  CK(cudaIpcGetMemHandle(&p.planes, h->planes));
+  CK(cudaIpcGetMemHandle(&p.y0s, h->y0s));
+  CK(cudaIpcGetMemHandle(&p.aeqs, h->aeqs));
+  p.plane = (long long)h->G.pitch * h->G.ny;
+  p.shift = PLANE_SHIFT;
+  p.pitch = h->G.pitch;
+  p.nxl = h->G.nxl;
+  p.ny = h->G.ny;
+  p.magic = PEER_MAGIC;
+  memcpy(blob, &p, sizeof(p));
+  return WB_OK;
+}
+int wb_peer_ipc_open(wb_handle* h, const void* blob, wb_peer* out) {
+  if (!h || !blob || !out) return WB_E_ARG;
+  PeerIpc p;
+  memcpy(&p, blob, sizeof(p));
+  if (p.magic != PEER_MAGIC || h->n_ipc_open + 3 > 6) {
+    g_err = "wb_peer_ipc_open: not a wb_peer_ipc_export blob, or more than two peers";
+    return WB_E_ARG;
+  }
+  CK(cudaSetDevice(h->dev));
+  void *pl = nullptr, *y0 = nullptr, *ae = nullptr;
+  CK(cudaIpcOpenMemHandle(&pl, p.planes, cudaIpcMemLazyEnablePeerAccess));
+  h->ipc_open[h->n_ipc_open++] = pl;
+  CK(cudaIpcOpenMemHandle(&y0, p.y0s, cudaIpcMemLazyEnablePeerAccess));
+  h->ipc_open[h->n_ipc_open++] = y0;
+  CK(cudaIpcOpenMemHandle(&ae, p.aeqs, cudaIpcMemLazyEnablePeerAccess));
+  h->ipc_open[h->n_ipc_open++] = ae;
+  fill_peer(out, (double*)pl, (double*)y0, (double*)ae, p.plane, p.shift, p.pitch, p.nxl, p.ny);
+  return WB_OK;
+}
+// plain step: after wb_step_local, the halo of the step's output buffer into
+// the peers (on the handle's stream; then all-reduce -> wb_finalize)
+int wb_push_halo_next(wb_handle* h) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  if (h->peer[0].q[0][0] || h->peer[1].q[0][0])
+    k_push_halo<<<148, 256, 0, h->stream>>>(h->G, h->B, h->peer[0], h->peer[1], 1);
+  CK(cudaGetLastError());
+  return WB_OK;
+}
+int wb_set_peers(wb_handle* h, const wb_peer* left, const wb_peer* right) {
+  if (!h) return WB_E_ARG;
+  CK(cudaSetDevice(h->dev));
+  CK(cudaStreamSynchronize(h->stream));
+  if (h->edge) CK(cudaStreamSynchronize(h->edge));
+  const wb_peer* src[2] = {left, right};
+  for (int s = 0; s < 2; s++) {
+    PeerBufs& d = h->peer[s];
+    memset(&d, 0, sizeof(d));
+    if (!src[s]) continue;
+    if (src[s]->ny != h->G.ny) {
+      g_err = "wb_set_peers: the neighbour slab has another number of rows";
+      return WB_E_ARG;
+    }
+    // a peer on another device: enable access to it (a no-op for IPC
+    // allocations, opened with cudaIpcMemLazyEnablePeerAccess)
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, src[s]->q[0][0]) == cudaSuccess && a.device != h->dev &&
+        a.device >= 0) {
+      cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        g_err = "wb_set_peers: no peer access to the neighbour's device";
+        return WB_E_CUDA;
+      }
+      cudaGetLastError();
+    }
+    for (int b = 0; b < 2; b++) {
+      for (int m = 0; m < 4; m++) d.q[b][m] = (double*)src[s]->q[b][m];
+      d.y0s[b] = (double*)src[s]->y0s[b];
+      d.aeqs[b] = (double*)src[s]->aeqs[b];
+    }
+    d.pitch = src[s]->pitch;
+    d.nxl = src[s]->nxl;
+  }
+  return WB_OK;
+}
+
 // Kernel-level timing with CUDA events on the handle's stream: n steps
 // launched individually, average duration of the detect and step kernels.
 int wb_profile_steps(wb_handle* h, int32_t n, double* ms_detect, double* ms_step,

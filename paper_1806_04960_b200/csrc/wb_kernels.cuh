@@ -70,6 +70,15 @@ struct Bufs {
   long long dtlog_cap;
 };
 
+// An x-neighbour slab's buffers as seen from this device (k_push_halo);
+// q[0][0] == nullptr: no neighbour on that side
+struct PeerBufs {
+  double* q[2][4];
+  double* y0s[2];
+  double* aeqs[2];
+  int pitch, nxl;
+};
+
 // Debug outputs in the reference layout (owned columns, (nxl, ny, 5))
 // Column-strip partition of one step launch: launch-local strip k is global
 // strip bx0 + k*bxs; tslot picks the ticket counter (two launches of one step

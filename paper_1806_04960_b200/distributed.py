@@ -8,7 +8,9 @@ all stream-ordered on the slab's CUDA stream (no host synchronisation):
     wb_step_local     detect + fused step kernel + [enc(errkey), rate] vector
     all_reduce(MAX)   -> globally first failing cell and the global CFL rate
     wb_finalize       commit (or stop) identically on every rank
-    halo exchange     pack edge columns, send/recv to x-neighbours, unpack
+    halo exchange     the edge columns stored into the neighbours' halo over
+                      peer memory (before the all-reduce), or pack, send/recv
+                      to the x-neighbours, unpack
 
 Results are bit-identical to a single-GPU run (tests/test_distributed_cpu.py
 runs the same driver over gloo with the CPU oracle as the slab backend).
@@ -139,6 +141,40 @@ class DeviceSlab:
                                              ctypes.c_void_p(self.send.data_ptr())),
                         "wb_step_begin")
 
+    # -- halo over peer memory (wb_set_peers) --
+    def peer_desc(self):
+        """This slab's buffers (wb_peer) for a neighbour in the same process."""
+        p = self._lib.WbPeer()
+        self._lib.check(self.L.wb_peer_desc(self.h, ctypes.byref(p)), "wb_peer_desc")
+        return p
+
+    def peer_export(self):
+        """This slab's buffers as a CUDA IPC blob for another process."""
+        b = ctypes.create_string_buffer(self._lib.WB_PEER_IPC_BYTES)
+        self._lib.check(self.L.wb_peer_ipc_export(self.h, b), "wb_peer_ipc_export")
+        return bytes(b.raw)
+
+    def peer_open(self, blob):
+        """A neighbour's exported buffers, opened on this slab's device."""
+        p = self._lib.WbPeer()
+        b = ctypes.create_string_buffer(bytes(blob), self._lib.WB_PEER_IPC_BYTES)
+        self._lib.check(self.L.wb_peer_ipc_open(self.h, b, ctypes.byref(p)), "wb_peer_ipc_open")
+        return p
+
+    def set_peers(self, left, right):
+        self._lib.check(self.L.wb_set_peers(self.h, ctypes.byref(left) if left else None,
+                                            ctypes.byref(right) if right else None),
+                        "wb_set_peers")
+        self.peers = (left, right)  # keep the descriptors alive
+
+    def step_begin_peer(self, max_dt, t_end, mode):
+        self._lib.check(self.L.wb_step_begin_peer(self.h, math.nan if max_dt is None else max_dt,
+                                                  0.0 if t_end is None else t_end, mode),
+                        "wb_step_begin_peer")
+
+    def push_halo_next(self):
+        self._lib.check(self.L.wb_push_halo_next(self.h), "wb_push_halo_next")
+
     def unpack_halo_next(self, have_left, have_right):
         self._lib.check(self.L.wb_unpack_halo_next(self.h, ctypes.c_void_p(self.recv.data_ptr()),
                                                    int(have_left), int(have_right)),
@@ -214,7 +250,8 @@ class DistributedSimulation:
     torch.distributed process group (the reference's Simulation semantics:
     same dt sequence, same error step/cell, bit-identical state)."""
 
-    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=True, graphs=True):
+    def __init__(self, backend, grid, cfl=0.45, group=None, overlap=True, graphs=True,
+                 halo=None):
         import torch.distributed as dist
         self.dist = dist
         self.be = backend
@@ -239,6 +276,44 @@ class DistributedSimulation:
         # set to False after a failed capture (then steps are enqueued eagerly)
         self.use_graphs = graphs and self._nccl and hasattr(backend, "stream")
         self._graphs = {}
+        # halo exchange: "peer" -- the step kernel's boundary columns stored by
+        # one kernel straight into the neighbours' halo (NVLink stores between
+        # GPUs, CUDA IPC between processes; the default for device slabs), or
+        # "collective" -- pack, send/recv through torch.distributed, unpack
+        if halo is None:
+            halo = os.environ.get("WB_HALO", "peer" if hasattr(backend, "peer_export")
+                                  else "collective")
+        if halo not in ("peer", "collective"):
+            raise ValueError(f"halo must be 'peer' or 'collective', not {halo!r}")
+        self.halo = halo
+        if halo == "peer":
+            self._setup_peers()
+
+    def _setup_peers(self):
+        """Every rank exports its buffers (CUDA IPC), gathers the others' and
+        opens its x-neighbours' on its device; falls back to the collective
+        exchange (with a warning) where peer access is unavailable."""
+        be, r, W = self.be, self.rank, self.world
+        try:
+            blobs = [None] * W
+            self.dist.all_gather_object(blobs, be.peer_export(), group=self.group)
+            left = be.peer_open(blobs[r - 1]) if r > 0 else None
+            right = be.peer_open(blobs[r + 1]) if r < W - 1 else None
+            be.set_peers(left, right)
+            ok = 1
+        except Exception as e:  # noqa: BLE001 -- reported, then the other path
+            import warnings
+            warnings.warn(f"halo over peer memory unavailable ({e}); using send/recv")
+            ok = 0
+        # every rank must take the same path
+        import torch
+        t = torch.tensor([ok], dtype=torch.int64,
+                         device=be.red.device if self._nccl else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(t.item()) == 0:
+            if ok:
+                be.set_peers(None, None)
+            self.halo = "collective"
 
     # -- collectives ------------------------------------------------------
     def _allreduce_max(self, t):
@@ -310,6 +385,19 @@ class DistributedSimulation:
     def _enqueue_step(self, max_dt=None, t_end=None):
         be = self.be
         mode = 1 if t_end is not None else 0
+        if self.halo == "peer":
+            # the halo goes into the neighbours' step output buffers before the
+            # all-reduce, which orders it before any rank's next step
+            with self._ctx():
+                if self.overlap:
+                    be.step_begin_peer(max_dt, t_end, mode)  # edges + peer stores on edge
+                    be.step_end()
+                else:
+                    be.step_local(max_dt, t_end, mode)
+                    be.push_halo_next()
+                self._allreduce_max(be.red)
+                be.finalize()
+            return
         if self.overlap:
             with self._ctx():
                 be.step_begin(max_dt, t_end, mode)  # interior here, edges + pack on edge

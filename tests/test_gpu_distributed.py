@@ -18,8 +18,12 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("overlap,graphs", [(False, False), (False, True), (True, True)])
-def test_nccl_world1_matches_simulation(overlap, graphs):
+@pytest.mark.parametrize("overlap,graphs,halo", [(False, False, "collective"),
+                                                 (False, True, "collective"),
+                                                 (True, True, "collective"),
+                                                 (True, True, "peer"),
+                                                 (False, True, "peer")])
+def test_nccl_world1_matches_simulation(overlap, graphs, halo):
     """NCCL world 1 (halo exchange skipped, all-reduce real): plain and
     overlapped steps, eager and CUDA-graph-captured chunks, equal the
     single-domain Simulation bit for bit; run_until twice and a later
@@ -40,7 +44,8 @@ def test_nccl_world1_matches_simulation(overlap, graphs):
         lo, hi = stored_range(res[0], i0, i1)
         sc = build_scenario("wall-impact", res, columns=(lo, hi))
         be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
-        dsim = DistributedSimulation(be, sc.grid, overlap=overlap, graphs=graphs)
+        dsim = DistributedSimulation(be, sc.grid, overlap=overlap, graphs=graphs, halo=halo)
+        assert dsim.halo == halo
         dsim.run_steps(25, check_every=8)
         assert dsim.use_graphs == graphs  # the capture worked
         full = build_scenario("wall-impact", res)
@@ -65,7 +70,7 @@ def test_nccl_world1_matches_simulation(overlap, graphs):
         dist.destroy_process_group()
 
 
-def _gloo_worker(rank, world, port, scen, res, steps, out, overlap):
+def _gloo_worker(rank, world, port, scen, res, steps, out, overlap, halo="collective"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch.distributed as dist
@@ -79,7 +84,8 @@ def _gloo_worker(rank, world, port, scen, res, steps, out, overlap):
     lo, hi = stored_range(res[0], i0, i1)
     sc = build_scenario(scen, res, columns=(lo, hi))
     be = DeviceSlab(sc.grid, sc.params, sc.q0, lo, sc.boundary, 0.45, i0, i1, 0)
-    dsim = DistributedSimulation(be, sc.grid, overlap=overlap)
+    dsim = DistributedSimulation(be, sc.grid, overlap=overlap, halo=halo)
+    assert dsim.halo == halo  # peer: CUDA IPC between the two processes worked
     err = None
     try:
         dsim.run_steps(steps, check_every=7)
@@ -91,14 +97,20 @@ def _gloo_worker(rank, world, port, scen, res, steps, out, overlap):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("scen,res,steps,overlap", [("wall-impact", (300, 160), 25, True),
-                                                    ("wall-impact", (300, 160), 25, False),
-                                                    ("dambreak-dry", (200, 100), 400, True)])
-def test_device_slabs_two_processes_gloo(scen, res, steps, overlap):
+@pytest.mark.parametrize("scen,res,steps,overlap,halo", [
+    ("wall-impact", (300, 160), 25, True, "collective"),
+    ("wall-impact", (300, 160), 25, False, "collective"),
+    ("dambreak-dry", (200, 100), 400, True, "collective"),
+    ("wall-impact", (900, 96), 25, True, "peer"),
+    ("wall-impact", (300, 160), 25, False, "peer"),
+    ("dambreak-dry", (200, 100), 400, True, "peer")])
+def test_device_slabs_two_processes_gloo(scen, res, steps, overlap, halo):
     """The full multi-process driver (torch.distributed, two ranks, device
     slabs on cuda:0, collectives staged through host memory by gloo) against
     the single-handle Simulation: same state, t and step; on the dry dambreak
-    the same abort (step 309, cell (98, 37)) on both ranks."""
+    the same abort (step 309, cell (98, 37)) on both ranks.  halo="peer":
+    the boundary columns go straight into the other process's buffers (CUDA
+    IPC), ordered by the host-staged all-reduce."""
     import tempfile
     import torch
     import torch.multiprocessing as mp
@@ -108,7 +120,7 @@ def test_device_slabs_two_processes_gloo(scen, res, steps, overlap):
     from paper_1806_04960_b200.scenarios import build_scenario
     from paper_1806_04960_b200.timestepper import Simulation
     out = tempfile.mkdtemp()
-    mp.spawn(_gloo_worker, args=(2, _port(), scen, res, steps, out, overlap), nprocs=2,
+    mp.spawn(_gloo_worker, args=(2, _port(), scen, res, steps, out, overlap, halo), nprocs=2,
              join=True)
     parts = [np.load(os.path.join(out, f"rank{r}.npz")) for r in range(2)]
     full = build_scenario(scen, res)

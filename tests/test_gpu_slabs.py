@@ -71,7 +71,15 @@ def _exchange(torch, slabs):
     torch.cuda.synchronize()
 
 
-def _run(torch, slabs, steps, overlap=False):
+def _set_peers(slabs):
+    """Halo over peer memory between the slabs (same GPU, direct pointers)."""
+    W = len(slabs)
+    for r, s in enumerate(slabs):
+        s.set_peers(slabs[r - 1].peer_desc() if r > 0 else None,
+                    slabs[r + 1].peer_desc() if r < W - 1 else None)
+
+
+def _run(torch, slabs, steps, overlap=False, peer=False):
     """Drive the slabs like distributed.DistributedSimulation: either
     step_local -> all-reduce -> finalize -> halo exchange, or the overlapped
     step_begin (edge strips + pack on the edge stream, interior strips on the
@@ -87,7 +95,20 @@ def _run(torch, slabs, steps, overlap=False):
         assert s.check_prepare()[1] == 0
     W = len(slabs)
     for _ in range(steps):
-        if overlap:
+        if peer:
+            # edges + peer halo stores, interior; the emulated all-reduce (a
+            # device synchronisation) orders the stores before the next step
+            for s in slabs:
+                if overlap:
+                    s.step_begin_peer(None, None, 0)
+                    s.step_end()
+                else:
+                    s.step_local(None, None, 0)
+                    s.push_halo_next()
+            _reduce(torch, slabs)
+            for s in slabs:
+                s.finalize()
+        elif overlap:
             for s in slabs:
                 s.step_begin(None, None, 0)
             _exchange(torch, slabs)
@@ -152,6 +173,33 @@ def test_device_slabs_overlapped_bitexact(torch_cuda, oracle, world):
 def test_device_slabs_overlapped_error_stop(torch_cuda):
     slabs = _slabs(torch_cuda, "dambreak-dry", (200, 100), 2)
     errs = _run(torch_cuda, slabs, 400, overlap=True)
+    assert errs is not None
+    for code, key, step, _ in errs:
+        assert (code, divmod(key, 100), step) == (4, (98, 37), 309)
+
+
+@pytest.mark.parametrize("world,overlap", [(2, True), (3, True), (3, False)])
+def test_device_slabs_peer_halo_bitexact(torch_cuda, oracle, world, overlap):
+    """Halo over peer memory: each slab's step stores its boundary columns
+    straight into the neighbours' halo (k_push_halo), with a real edge /
+    interior split; bit-identical to the single-domain oracle."""
+    from paper_1806_04960_b200.scenarios import build_scenario
+    res = (400 * world, 96)
+    slabs = _slabs(torch_cuda, "wall-impact", res, world)
+    _set_peers(slabs)
+    assert _run(torch_cuda, slabs, 12, overlap=overlap, peer=True) is None
+    q = np.concatenate([s.owned_state() for s in slabs], axis=0)
+    sc = build_scenario("wall-impact", res)
+    ref = oracle.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
+    ref.run_steps(12)
+    assert np.array_equal(q, ref.q)
+    assert all(s.status()["t"] == ref.t for s in slabs)
+
+
+def test_device_slabs_peer_halo_error_stop(torch_cuda):
+    slabs = _slabs(torch_cuda, "dambreak-dry", (200, 100), 2)
+    _set_peers(slabs)
+    errs = _run(torch_cuda, slabs, 400, overlap=True, peer=True)
     assert errs is not None
     for code, key, step, _ in errs:
         assert (code, divmod(key, 100), step) == (4, (98, 37), 309)
