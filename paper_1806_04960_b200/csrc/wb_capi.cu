@@ -241,7 +241,20 @@ static cudaError_t step_attr() {
                               cudaFuncAttributePreferredSharedMemoryCarveout,
                               (int)cudaSharedmemCarveoutMaxShared);
 }
+template <int NTV, int MB, bool G1>
+static cudaError_t push_attr() {
+  cudaError_t e = cudaFuncSetAttribute(k_step_push<NTV, MB, G1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       step_smem_bytes<NTV>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_step_push<NTV, MB, G1>,
+                              cudaFuncAttributePreferredSharedMemoryCarveout,
+                              (int)cudaSharedmemCarveoutMaxShared);
+}
 static int init_step_kernels() {
+  CK((push_attr<128, 3, true>()));
+  CK((push_attr<64, 1, true>()));
+  CK((push_attr<64, 1, false>()));
   CK((step_attr<64, 1, true, false>()));
   CK((step_attr<64, 1, true, true>()));
   CK((step_attr<64, 1, false, false>()));
@@ -283,9 +296,17 @@ static int step_nt(const wb_handle* h, bool debug) {
 // the interior strips (run concurrently with the edge strips' halo exchange).
 enum { PART_ALL = 0, PART_EDGE = 1, PART_INTERIOR = 2 };
 
+// whether the edge launch can store the halo into the peers itself
+// (k_step_push is built for the default variants; tiny slabs, whose two
+// halo-source column pairs overlap, use k_push_halo)
+static bool edge_push_built(const wb_handle* h) {
+  return (h->peer[0].q[0][0] || h->peer[1].q[0][0]) && h->G.nxl >= 2 * HALO &&
+         (!h->g1 || h->variant == 0 || h->variant == 3);
+}
+
 template <bool DEBUG>
 static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
-                        int which = PART_ALL) {
+                        int which = PART_ALL, bool push = false) {
   if (!s) s = h->stream;
   const Geo& G = h->G;
   const int nt = step_nt(h, DEBUG);
@@ -308,6 +329,16 @@ static void launch_step(wb_handle* h, const Dbg& D, cudaStream_t s = nullptr,
 #define WB_LAUNCH(K, NTV)                                                          \
   K<<<g, NTV, step_smem_bytes<NTV>(), s>>>(G, h->B, h->P, h->L, D, part, h->tq[NTV / 32 - 1], \
                                           h->tm[NTV / 32 - 1])
+#define WB_LAUNCH_PUSH(K, NTV)                                                             \
+  K<<<g, NTV, step_smem_bytes<NTV>(), s>>>(G, h->B, h->P, h->L, D, part, h->tq[NTV / 32 - 1], \
+                                          h->tm[NTV / 32 - 1], h->peer[0], h->peer[1])
+  if (!DEBUG && push) {  // the slab-edge launch, storing the halo into the peers
+    if (!h->g1) WB_LAUNCH_PUSH((k_step_push<64, 1, false>), 64);
+    else if (h->variant == 3) WB_LAUNCH_PUSH((k_step_push<128, 3, true>), 128);
+    else WB_LAUNCH_PUSH((k_step_push<64, 1, true>), 64);
+    return;
+  }
+#undef WB_LAUNCH_PUSH
   if (!h->g1) {
     WB_LAUNCH((k_step<64, 1, false, DEBUG>), 64);
     return;
@@ -1182,7 +1213,10 @@ static int step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, v
   k_reset_counters<<<1, 1, 0, h->stream>>>(h->st);
   CK(cudaEventRecord(h->ev_fork, h->stream));
   CK(cudaStreamWaitEvent(h->edge, h->ev_fork, 0));
-  launch_step<false>(h, Dbg{}, h->edge, PART_EDGE);
+  // halo over peer memory with the default variants: the edge launch stores
+  // its halo-source columns into the peers as it produces them
+  const bool fused = !send && edge_push_built(h);
+  launch_step<false>(h, Dbg{}, h->edge, PART_EDGE, fused);
   {
     // a split edge launch leaves the detection of its strips' owned columns
     // to k_detect_cols (see launch_step); the pack needs it for the halo
@@ -1193,12 +1227,17 @@ static int step_begin(wb_handle* h, double max_dt, double t_end, int32_t mode, v
       const int c0 = HALO, c1 = std::min(HALO + w, h->G.nxl + HALO);
       const int c2 = ((int)g.x - 1) * w + HALO, c3 = std::min(c2 + w, h->G.nxl + HALO);
       const int ncols = (c1 - c0) + (c3 - c2);
-      k_detect_cols<<<(ncols + 7) / 8, 256, 0, h->edge>>>(h->G, h->B, h->P.dy, c0, c1, c2, c3);
+      // (fused: it also stores the detection of the halo-source columns
+      // into the peers)
+      const PeerBufs none{};
+      k_detect_cols<<<(ncols + 7) / 8, 256, 0, h->edge>>>(
+          h->G, h->B, h->P.dy, c0, c1, c2, c3, fused ? h->peer[0] : none,
+          fused ? h->peer[1] : none);
     }
   }
   if (send)
     k_pack_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, (double*)send, 1);
-  else if (h->peer[0].q[0][0] || h->peer[1].q[0][0])
+  else if (!fused && (h->peer[0].q[0][0] || h->peer[1].q[0][0]))
     k_push_halo<<<148, 256, 0, h->edge>>>(h->G, h->B, h->peer[0], h->peer[1], 1);
   launch_step<false>(h, Dbg{}, h->stream, PART_INTERIOR);
   CK(cudaGetLastError());

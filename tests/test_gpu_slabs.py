@@ -203,3 +203,20 @@ def test_device_slabs_peer_halo_error_stop(torch_cuda):
     assert errs is not None
     for code, key, step, _ in errs:
         assert (code, divmod(key, 100), step) == (4, (98, 37), 309)
+
+
+def test_device_slabs_peer_halo_fused_chain(torch_cuda, oracle):
+    """Slabs of two column strips (no edge/interior split) with long columns
+    (ny >= 2048: the detection is chained inside the step kernel): the edge
+    launch is the whole step, and its last row segment stores the halo
+    columns' detection into the neighbours along with the state."""
+    from paper_1806_04960_b200.scenarios import build_scenario
+    res = (200, 2048)
+    slabs = _slabs(torch_cuda, "wall-impact", res, 2)
+    _set_peers(slabs)
+    assert _run(torch_cuda, slabs, 10, overlap=True, peer=True) is None
+    q = np.concatenate([s.owned_state() for s in slabs], axis=0)
+    sc = build_scenario("wall-impact", res)
+    ref = oracle.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
+    ref.run_steps(10)
+    assert np.array_equal(q, ref.q)
