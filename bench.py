@@ -488,10 +488,11 @@ def run_ours_distributed(args):
                                + f" + one {backend} MAX all-reduce per step"
                                + (", edge strips overlapped" if overlapped else "")
                                + (", CUDA graph of the step sequence" if graphs_used else ""),
-                # per overlapped step: set_run, reset_counters, k_step (edge strips),
-                # k_detect_cols, k_step (interior), prefinalize, finalize, and the
-                # halo: k_push_halo (peer) or k_pack_halo + k_unpack_halo
-                "gpu_launches": (8 if halo_mode == "peer" else 9) * args.steps,
+                # per overlapped step: set_run, reset_counters, the edge strips
+                # (k_step_push, which stores the halo into the peers, or k_step),
+                # k_detect_cols, k_step (interior), prefinalize, finalize, and for
+                # the collective halo k_pack_halo + k_unpack_halo
+                "gpu_launches": (7 if halo_mode == "peer" else 9) * args.steps,
                 "roofline": roof, "cpu_baseline": None,
                 "e2e": {"value": n_fluid * args.steps / wall, "unit": UNIT,
                         "h2d_bytes_per_step": state_bytes / args.steps,
