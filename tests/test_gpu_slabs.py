@@ -220,3 +220,26 @@ def test_device_slabs_peer_halo_fused_chain(torch_cuda, oracle):
     ref = oracle.OracleSimulation(sc.grid, sc.params, sc.q0, sc.boundary)
     ref.run_steps(10)
     assert np.array_equal(q, ref.q)
+
+
+def test_device_slabs_peer_halo_gamma7_matches_collective(torch_cuda):
+    """gamma != 1 (pow; the 64-thread gamma != 1 edge kernel stores the halo
+    into the peers): slabs with the peer-memory halo equal, bit for bit, the
+    same slabs with the packed halo exchange (the arithmetic is the same; only
+    the halo transport differs), and the single-handle Simulation."""
+    import numpy as np
+    from paper_1806_04960_b200.scenarios import build_scenario
+    from paper_1806_04960_b200.timestepper import Simulation
+    res = (400, 32)
+    a = _slabs(torch_cuda, "tait7", res, 2)
+    b = _slabs(torch_cuda, "tait7", res, 2)
+    _set_peers(a)
+    assert _run(torch_cuda, a, 6, overlap=True, peer=True) is None
+    assert _run(torch_cuda, b, 6, overlap=True) is None
+    qa = np.concatenate([s.owned_state() for s in a], axis=0)
+    qb = np.concatenate([s.owned_state() for s in b], axis=0)
+    assert np.array_equal(qa.view(np.uint64), qb.view(np.uint64))
+    sc = build_scenario("tait7", res)
+    sim = Simulation(sc.grid, sc.params, sc.q0, sc.boundary)
+    sim.run_steps(6)
+    assert np.array_equal(qa.view(np.uint64), sim.q.view(np.uint64))
